@@ -1,0 +1,68 @@
+// common.cuh -- shared host/device definitions of the NTC CUDA path (product code).
+#pragma once
+#include <cstdint>
+
+#include "../../include/ntc.h"
+
+namespace ntc {
+
+constexpr int HID = 64;          // hidden width
+constexpr int MAX_MIPS = 16;     // W <= 2^15
+constexpr int MAX_LEVELS = 8;
+constexpr int TILE_M = 128;      // texels per tcgen05 tile (MMA M)
+constexpr int NWG = 4;           // warpgroups per decode CTA, each owns a tile pipeline
+
+__host__ __device__ constexpr int pow2_bytes(int bits) {
+    return bits <= 8 ? 1 : bits <= 16 ? 2 : bits <= 32 ? 4 : bits <= 64 ? 8 : 16;
+}
+
+// Compile-time profile (Table 2): C0 x B0 and C1 x B1 latents, input width D.
+template <int C0_, int B0_, int C1_, int B1_>
+struct Prof {
+    static constexpr int C0 = C0_, B0 = B0_, C1 = C1_, B1 = B1_;
+    static constexpr int D = 4 * C0 + C1 + 12 + 1;
+    static constexpr int K1 = ((D + 1 + 15) / 16) * 16;  // + the constant-1 bias column
+    static constexpr int K1W = K1 / 2;                   // fp16 pairs
+    static constexpr int K1_ATOMS = (K1 + 63) / 64;      // 64-wide SW128 atoms along K
+    static constexpr int CELL0 = pow2_bytes(C0 * B0);    // packed cell bytes
+    static constexpr int CELL1 = pow2_bytes(C1 * B1);
+    static_assert((C0 % 2) == 0 && (C1 % 2) == 0, "even channel counts");
+    static_assert(32 % B0 == 0 && 32 % B1 == 0, "bits must divide 32");
+};
+
+// Per-level geometry for the device: resolutions and byte offsets into the packed grids.
+struct LevelGeom {
+    int32_t r0, r1;
+    int64_t off0, off1;  // byte offsets of packed G0 / G1 of this level
+};
+
+// Everything a decode launch needs, passed by value (param space / constant bank).
+struct DecodeParams {
+    const uint8_t* grids;
+    const uint4* wimg;        // global copy of the SMEM weight image
+    uint32_t wimg_bytes;
+    int32_t W, c, M, L;
+    int32_t mode;             // 0: tiles over mips, 1: queries, 2: debug assemble
+    LevelGeom lv[MAX_LEVELS];
+    int8_t level_of[MAX_MIPS];
+    uint32_t lod_word[MAX_MIPS];  // half(lod) | half(1.0) << 16
+    uint32_t pe_words[8][4];      // PE of one axis at p = x mod 8, as 3 half2 words (+pad)
+    // mode 0
+    int32_t mip_first, mip_count;
+    int64_t tile_start[MAX_MIPS + 1];
+    int64_t out_off[MAX_MIPS];     // element offset of mip in out
+    int64_t row_stride[MAX_MIPS];  // elements
+    int64_t n_tiles;
+    // mode 1 / 2
+    const ntc_query* q;
+    int64_t nq;
+    int32_t* status;
+    int32_t* dbg_addr;
+    uint16_t* dbg_X;
+    uint16_t* out;
+    float b2[HID];
+    float b2b[HID];
+    float b3[16];
+};
+
+}  // namespace ntc

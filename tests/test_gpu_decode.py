@@ -1,0 +1,212 @@
+"""GPU parity of the decode path (a0..a7) against the CPU oracle, through the C ABI.
+
+Bars (BASELINE.json north_star): bit-exact addressing, quantised codes and assembled fp16
+inputs; max abs error <= 2e-3 on decoded channels in [0, 1].
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2305_17105_b200 as ntc
+from paper_2305_17105_b200.synth import Profile, gen_latents, gen_queries
+from helpers import chain_queries, material_inputs
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+DEV = "cuda:0"
+
+
+def _material(O, d, seed, out_gain=0.3):
+    codes, w = material_inputs(O, d, seed, out_gain)
+    mat = ntc.Material(d, torch.from_numpy(codes).to(DEV), torch.from_numpy(w.view(np.int16)).to(DEV))
+    return mat, codes, w
+
+
+def _decode_queries_gpu(mat, xym):
+    q = ntc.pack_queries(torch.from_numpy(xym).to(DEV))
+    out = torch.empty((xym.shape[0], mat.desc.channels), dtype=torch.float16, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ntc.ntc_decode_texels(mat, q, out, st)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy(), int(st.item())
+
+
+@pytest.mark.parametrize("name", ["ntc0.2", "ntc0.5", "ntc1.0", "ntc2.25"])
+def test_quantize_bit_exact(O, name):
+    """a0: codes bit-exact, including exact ties at every bin edge and out-of-range values."""
+    d = Profile.named(name, 256, 8)
+    n = O.num_latents(d)
+    lat = gen_latents(5, n, scale=0.7)
+    # plant exact ties (bin edges (idx + 1/2) Q) in both grids' bit depths
+    rng = np.random.default_rng(0)
+    for B in {d.b0, d.b1}:
+        N = 2**B
+        idx = rng.choice(n, 2000, replace=False)
+        lat[idx] = ((rng.integers(-N // 2, N // 2 + 1, idx.size) + 0.5) / N).astype(np.float32)
+    want = O.quantize_latents(d, lat)
+    codes = torch.empty(n, dtype=torch.uint8, device=DEV)
+    ntc.ntc_quantize_latents(d, torch.from_numpy(lat).to(DEV), codes)
+    assert np.array_equal(codes.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name", ["ntc0.2", "ntc0.5", "ntc1.0", "ntc2.25"])
+def test_assemble_bit_exact(O, name):
+    """a1-a4: addressing and the fp16 input vector X bit-exact vs the oracle, every mip."""
+    W = 128
+    d = Profile.named(name, W, 8)
+    mat, codes, _ = _material(O, d, 21)
+    xym = chain_queries(W, range(O.num_mips(W)), stride=1)
+    xym = xym[np.random.default_rng(1).permutation(xym.shape[0])[:6000]]
+    q = ntc.pack_queries(torch.from_numpy(xym).to(DEV))
+    n = xym.shape[0]
+    addr = torch.empty((n, 17), dtype=torch.int32, device=DEV)
+    X = torch.empty((n, d.input_dim), dtype=torch.int16, device=DEV)
+    ntc.ntc_debug_assemble(mat, q, addr, X)
+    addr, X = addr.cpu().numpy(), X.cpu().numpy().view(np.uint16)
+    for i in range(n):
+        x, y, m = xym[i]
+        ti, _ = O.address(d, m, x, y)
+        assert np.array_equal(addr[i], ti), (x, y, m)
+        assert np.array_equal(X[i], O.assemble(d, codes, m, x, y)), (x, y, m)
+
+
+def test_decode_mip_c1(O):
+    """configs[0]: 256^2, 8 channels, mip 0, NTC 0.2, [57, 64, 64, 8]: every texel."""
+    d = Profile.named("ntc0.2", 256, 8)
+    mat, codes, w = _material(O, d, 0x4E544300)
+    out = torch.empty((256, 256, 8), dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_mip(mat, 0, out)
+    torch.cuda.synchronize()
+    ref = O.decode_mip(d, codes, w, 0)
+    err = np.abs(out.float().cpu().numpy() - ref)
+    assert err.max() <= TOL, err.max()
+
+
+@pytest.mark.parametrize("name,hm,c", [("ntc0.2", 1, 9), ("ntc0.2", 2, 9), ("ntc0.5", 1, 16), ("ntc1.0", 1, 3),
+                                        ("ntc2.25", 1, 12), ("ntc2.25", 2, 16)])
+def test_decode_chain_profiles(O, name, hm, c):
+    """Full chain (all mips incl. ragged tail tiles) for every compiled profile / depth."""
+    W = 128
+    d = Profile.named(name, W, c, hm)
+    mat, codes, w = _material(O, d, 7 + hm)
+    T = ntc.ntc_chain_texels(d)
+    out = torch.full((T * c,), float("nan"), dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_chain(mat, out)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for m in range(O.num_mips(W)):
+        wm = W >> m
+        off = ntc.ntc_mip_offset(d, m) * c
+        ref = O.decode_mip(d, codes, w, m).reshape(-1)
+        err = np.abs(got[off: off + wm * wm * c] - ref)
+        assert err.max() <= TOL, (m, err.max())
+
+
+def test_decode_chain_c2_full(O):
+    """configs[1]: 2048^2, 9 channels, full chain (5,592,405 texels): every texel."""
+    d = Profile.named("ntc0.2", 2048, 9)
+    mat, codes, w = _material(O, d, 0x4E544301)
+    T = ntc.ntc_chain_texels(d)
+    assert T == 5_592_405
+    out = torch.empty((T * 9,), dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_chain(mat, out)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for m in range(O.num_mips(2048)):
+        wm = 2048 >> m
+        off = ntc.ntc_mip_offset(d, m) * 9
+        ref = O.decode_mip(d, codes, w, m).reshape(-1)
+        err = np.abs(got[off: off + wm * wm * 9] - ref)
+        assert err.max() <= TOL, (m, err.max())
+
+
+def test_decode_stress_gain(O):
+    """Stress material: output gain 1.0 (about half the outputs clamped)."""
+    d = Profile.named("ntc0.2", 256, 16)
+    mat, codes, w = _material(O, d, 99, out_gain=1.0)
+    for m in (0, 1, 4, 8):
+        wm = 256 >> m
+        out = torch.empty((wm, wm, 16), dtype=torch.float16, device=DEV)
+        ntc.ntc_decode_mip(mat, m, out)
+        torch.cuda.synchronize()
+        err = np.abs(out.float().cpu().numpy() - O.decode_mip(d, codes, w, m))
+        assert err.max() <= TOL, (m, err.max())
+
+
+def test_decode_mip_row_stride(O):
+    d = Profile.named("ntc0.2", 64, 5)
+    mat, codes, w = _material(O, d, 3)
+    buf = torch.full((32, 200), -1.0, dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_mip(mat, 1, buf, row_stride_elems=200)
+    torch.cuda.synchronize()
+    got = buf.float().cpu().numpy()
+    assert np.all(got[:, 160:] == -1.0)
+    err = np.abs(got[:, :160].reshape(32, 32, 5) - O.decode_mip(d, codes, w, 1))
+    assert err.max() <= TOL
+
+
+def test_decode_texels_random_and_errors(O):
+    """configs[2]-style random access (area-uniform mips, random order), an empty batch,
+    and out-of-range queries (status bit + NaN row, the rest decoded normally)."""
+    d = Profile.named("ntc0.2", 512, 16)
+    mat, codes, w = _material(O, d, 0x4E544302)
+    xym = gen_queries(5, 512, 20000, "area")
+    xym2 = gen_queries(6, 512, 5000, "mip")
+    allq = np.concatenate([xym, xym2])
+    bad = np.array([[512, 0, 0], [0, 300, 1], [0, 0, 10], [3, 3, 40]], np.int32)
+    allq = np.concatenate([allq[:100], bad, allq[100:]])
+    got, st = _decode_queries_gpu(mat, allq)
+    assert st & ntc.NTC_ERR_OUT_OF_RANGE
+    assert np.all(np.isnan(got[100:104]))
+    ok = np.ones(allq.shape[0], bool)
+    ok[100:104] = False
+    ref = O.decode_texels(d, codes, w, allq[ok])
+    assert np.abs(got[ok] - ref).max() <= TOL
+    # empty batch is a no-op
+    empty = torch.empty(0, dtype=torch.int64, device=DEV)
+    ntc.ntc_decode_texels(mat, empty, torch.empty((0, 16), dtype=torch.float16, device=DEV))
+
+
+def test_invalid_arguments(O):
+    d = Profile.named("ntc0.2", 64, 8)
+    mat, _, _ = _material(O, d, 1)
+    out = torch.empty((64 * 64 * 8,), dtype=torch.float16, device=DEV)
+    with pytest.raises(ntc.NtcError) as e:
+        ntc.ntc_decode_mip(mat, 7, out)
+    assert e.value.status == ntc.NTC_ERR_INVALID_ARGUMENT
+    with pytest.raises(ntc.NtcError) as e:
+        ntc.ntc_decode_mip(mat, 0, out, row_stride_elems=10)
+    bad = Profile(64, 8, 4, 6, 3, 12, 4)
+    with pytest.raises(ntc.NtcError) as e:
+        ntc.Material(bad, torch.zeros(10, dtype=torch.uint8, device=DEV), torch.zeros(10, dtype=torch.int16, device=DEV))
+    assert e.value.status == ntc.NTC_ERR_UNSUPPORTED
+
+
+def test_smallest_texture(O):
+    """W = 8 (one feature level, G0 2x2, G1 1x1): the degenerate geometry."""
+    d = Profile.named("ntc0.2", 8, 4)
+    mat, codes, w = _material(O, d, 2)
+    T = ntc.ntc_chain_texels(d)
+    out = torch.empty((T * 4,), dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_chain(mat, out)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    ref = np.concatenate([O.decode_mip(d, codes, w, m).reshape(-1) for m in range(4)])
+    assert np.abs(got - ref).max() <= TOL
+
+
+def test_full_size_4k_sampled(O):
+    """configs[2] at full size in the bench launch configuration: 4096^2, 16 ch chain
+    decoded by one ntc_decode_chain launch; 200k sampled texels (all mips) vs the oracle."""
+    d = Profile.named("ntc0.2", 4096, 16)
+    mat, codes, w = _material(O, d, 0x4E544302)
+    T = ntc.ntc_chain_texels(d)
+    out = torch.empty((T * 16,), dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_chain(mat, out)
+    torch.cuda.synchronize()
+    xym = gen_queries(11, 4096, 200000, "mip")
+    offs = np.array([ntc.ntc_mip_offset(d, m) for m in range(13)], np.int64)
+    idx = offs[xym[:, 2]] + xym[:, 1].astype(np.int64) * (4096 >> xym[:, 2]) + xym[:, 0]
+    got = out.view(-1, 16)[torch.from_numpy(idx).to(DEV)].float().cpu().numpy()
+    ref = O.decode_texels(d, codes, w, xym)
+    assert np.abs(got - ref).max() <= TOL
