@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""NTC hot-path benchmark (BASELINE.json metric: decoded Gtexel/s on the 4K 9-channel
+full mip chain, and training texels/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the hot path over synthetic inputs resident in HBM:
+  decode  : ntc_decode_chain of a 4096^2, 9-channel, NTC 0.2 material (22,369,621 texels)
+  train   : ntc_train_step(GRADS|APPLY) on 4 random 256^2 crops at LOD 0 (262,144 texels)
+            of a 4096^2 9-channel material (configs[3]), when the library provides it.
+L2 is flushed (256 MiB write) before every timed step, outside the CUDA-event window.
+Multi-GPU (torchrun): weak scaling, one independent material per rank (configs[4]:
+decode needs no collective); time = max over ranks of the device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2305_17105_b200.synth import (SEED_BASE, Profile, box_mip_chain_u8, gen_codes, gen_crops,  # noqa: E402
+                                         gen_latents, gen_queries, gen_reference_u8, gen_weights_f16,
+                                         gen_weights_f32, u8_to_f16_bits)
+
+METRIC = "decoded Gtexel/s (4K 9-ch material, full mip chain) and training texels/s"
+UNIT = "Gtexel/s"
+W, C = 4096, 9
+WORKLOAD = "4096^2 x 9ch NTC0.2 [57,64,64,9] full-chain decode (22,369,621 texels)"
+TRAIN_WORKLOAD = "4096^2 x 9ch NTC0.2 train step, 4 x 256^2 crops at LOD 0 (262,144 texels)"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def _ncu_traffic(kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu summary (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and clock-event (throttle) reasons during the timed region."""
+
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+             0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+             0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def report(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unavailable"]}
+        rs = [n for b, n in self.NAMES.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max, "reasons": rs,
+                "samples": len(self.samples)}
+
+
+def decode_flops_per_texel(d):
+    """Unpadded algorithmic FLOPs per decoded texel: 2 (D*64 + 4096 h + 64 c)."""
+    return 2 * (d.input_dim * 64 + 4096 * d.hidden_mats + 64 * d.channels)
+
+
+def train_flops_per_texel(d):
+    """forward + dX (hidden, latent inputs) + dW."""
+    h = d.hidden_mats
+    fwd = d.input_dim * 64 + 4096 * h + 64 * d.channels
+    bwd = 64 * d.channels + 4096 * h + (4 * d.c0 + d.c1) * 64 + 64 * d.channels + 4096 * h + 64 * d.input_dim
+    return 2 * (fwd + bwd)
+
+
+# ------------------------------------------------------------------------------------ ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_17105_b200 as ntc
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    d = Profile.named("ntc0.2", W, C)
+    seed = SEED_BASE + 4 + rank  # configs[4]: per-material seed = base + material id
+    codes = gen_codes(seed, ntc.grid_list(d))
+    wts = gen_weights_f16(seed + 1, d.input_dim, C)
+    codes_d = torch.from_numpy(codes).to(dev)
+    w_d = torch.from_numpy(wts.view(np.int16)).to(dev)
+    mat = ntc.Material(d, codes_d, w_d)
+    T = ntc.ntc_chain_texels(d)
+    out = torch.empty((T * C,), dtype=torch.float16, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    # training state (configs[3]) if the library provides the step
+    train = None
+    try:
+        tr = ntc.Trainer(d)
+        NL, P = ntc.ntc_num_latents(d), ntc.ntc_num_params(d)
+        tb = {k: torch.zeros(NL, device=dev) for k in ("m_lat", "v_lat", "grad_lat", "noisy")}
+        tb.update({k: torch.zeros(P, device=dev) for k in ("m_par", "v_par", "grad_par")})
+        tb["latents"] = torch.from_numpy(gen_latents(seed + 2, NL)).to(dev)
+        tb["params"] = torch.from_numpy(gen_weights_f32(seed + 3, d.input_dim, C)).to(dev)
+        ref0 = torch.from_numpy(u8_to_f16_bits(gen_reference_u8(seed + 4, W, C)).view(np.int16)).to(dev)
+        train = dict(tr=tr, tb=tb, buf=ntc.make_buffers(tb), ref=ref0, loss=torch.zeros(1, device=dev),
+                     status=torch.zeros(1, dtype=torch.int32, device=dev))
+    except ntc.NtcError as e:
+        if e.status != ntc.NTC_ERR_UNSUPPORTED:
+            raise
+
+    def train_step(i):
+        crops = gen_crops(seed + 100 + i, W, 0, 4, 256)
+        batch = ntc.make_batch(0, crops, train["ref"], W * C)
+        hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, i + 1, seed, 1, 0)
+        ntc.ntc_train_step(train["tr"], train["buf"], batch, hp, train["loss"], train["status"])
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+    def step(i, timed):
+        flush.zero_()
+        ev[0].record(stream)
+        ntc.ntc_decode_chain(mat, out)
+        ev[1].record(stream)
+        if train is not None:
+            train_step(i)
+        ev[2].record(stream)
+        if timed:
+            ev[2].synchronize()
+            return (ev[0].elapsed_time(ev[2]) / 1e3, ev[0].elapsed_time(ev[1]) / 1e3,
+                    ev[1].elapsed_time(ev[2]) / 1e3)
+        return None
+
+    for i in range(args.warmup):
+        step(i, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tot = dec = trn = 0.0
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            a, b, c = step(args.warmup + i, True)
+            tot += a
+            dec += b
+            trn += c
+    torch.cuda.synchronize()
+    if world > 1:
+        t = torch.tensor([tot, dec, trn], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        tot, dec, trn = t.tolist()
+
+    texels = T * world * args.steps
+    res = {}
+    pk, pk_src = _peaks()
+    peak_tf = pk["bf16_tflops"]
+    dec_flops = decode_flops_per_texel(d) * T
+    achieved = dec_flops / (dec / args.steps) / 1e12
+    tr_bytes = _ncu_traffic("decode")
+    res.update({
+        "metric": METRIC, "value": texels / dec / 1e9, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16 (fp32 accumulate)",
+        "data": "synthetic (seeded iid codes, He-uniform fp16 weights; DESIGN.md input recipe)",
+        "config": {"workload": WORKLOAD, "profile": "ntc0.2", "width": W, "channels": C,
+                   "texels_per_step_per_gpu": T, "l2": "flushed (256 MiB write) before each timed step",
+                   "parallelism": f"material-parallel x{world} (no collective)"},
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak_tf, 4), "traffic": tr_bytes,
+                     "peak_source": f"{pk_src} bf16 dense burst (fp16 same rate)",
+                     "kernel": "ntc::decode_kernel", "flops_per_texel": decode_flops_per_texel(d)},
+        "gpu_launches": args.steps * (1 + (3 if train is not None else 0)),
+        "clocks": clk.report(),
+    })
+    if train is not None:
+        B = 4 * 256 * 256
+        tflops = train_flops_per_texel(d) * B / (trn / args.steps) / 1e12
+        res["train"] = {"metric": "training texels/s", "value": B * world * args.steps / trn,
+                        "unit": "texel/s", "ms_per_step": trn / args.steps * 1e3, "workload": TRAIN_WORKLOAD,
+                        "roofline": {"bound": "tensor", "achieved": round(tflops, 2), "peak": peak_tf,
+                                     "unit": "TFLOP/s", "frac": round(tflops / peak_tf, 4)}}
+    # e2e through the public API from pinned host buffers (rank 0 and every rank alike)
+    res["e2e"] = e2e(args, ntc, torch, d, codes, wts, dev, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(d, codes, wts, budget_s=args.cpu_budget)
+    return res
+
+
+def e2e(args, ntc, torch, d, codes, wts, dev, world):
+    """Same metric through the public API: H2D of the compressed material (codes + fp16
+    weights) from pinned memory, material create (pack), full-chain decode, D2H of the
+    decoded chain into pinned memory, every step."""
+    T = ntc.ntc_chain_texels(d)
+    h_codes = torch.from_numpy(codes).pin_memory()
+    h_w = torch.from_numpy(wts.view(np.int16)).pin_memory()
+    h_out = torch.empty((T * d.channels,), dtype=torch.float16).pin_memory()
+    d_codes = torch.empty_like(h_codes, device=dev)
+    d_w = torch.empty_like(h_w, device=dev)
+    d_out = torch.empty((T * d.channels,), dtype=torch.float16, device=dev)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(1, min(args.steps, 10))
+    tot = 0.0
+    for i in range(steps + 1):
+        e0.record(s)
+        d_codes.copy_(h_codes, non_blocking=True)
+        d_w.copy_(h_w, non_blocking=True)
+        m = ntc.Material(d, d_codes, d_w)
+        ntc.ntc_decode_chain(m, d_out)
+        h_out.copy_(d_out, non_blocking=True)
+        e1.record(s)
+        e1.synchronize()
+        m.close()
+        if i > 0:
+            tot += e0.elapsed_time(e1) / 1e3
+    return {"value": T * world * steps / tot / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": int(h_codes.numel() + 2 * h_w.numel()),
+            "d2h_bytes_per_step": int(2 * h_out.numel()),
+            "note": "decode via ntc_material_create + ntc_decode_chain, host-pinned in/out"}
+
+
+# ------------------------------------------------------------------------------------ oracle
+def _oracle_decode_sample(O, d, codes, wts, n, seed):
+    q = gen_queries(seed, W, n, "area")
+    t0 = time.perf_counter()
+    O.decode_texels(d, codes, wts, q, nthreads=0)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(d, codes, wts, budget_s=15.0):
+    import oracle as O
+
+    O.build()
+    n, el = 1 << 14, 0.0
+    while True:
+        el = _oracle_decode_sample(O, d, codes, wts, n, 77)
+        if el >= budget_s / 3 or n >= (1 << 24):
+            break
+        n *= 2
+    cores = os.cpu_count()
+    return {"value": n / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} area-uniform random texels of the 4096^2 9ch chain, oracle decode_texels "
+                      f"(C fp64, OpenMP {cores} threads), {el:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on the host cores, same metric/config."""
+    if rank != 0:
+        return None
+    import oracle as O
+
+    O.build()
+    d = Profile.named("ntc0.2", W, C)
+    grids = []
+    for j in range(O.num_levels(d)):
+        r0, r1 = O.grid_res(d, j)
+        grids += [(r0 * r0 * d.c0, d.b0), (r1 * r1 * d.c1, d.b1)]
+    codes = gen_codes(SEED_BASE + 4, grids)
+    wts = gen_weights_f16(SEED_BASE + 5, d.input_dim, C)
+    n = 1 << 16
+    for i in range(args.warmup):
+        _oracle_decode_sample(O, d, codes, wts, n, 1000 + i)
+    tot = 0.0
+    for i in range(args.steps):
+        tot += _oracle_decode_sample(O, d, codes, wts, n, 2000 + i)
+    v = n * args.steps / tot / 1e9
+    cores = os.cpu_count()
+    return {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD + f" (bounded sample: {n} texels/step)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{n} area-uniform random texels per step, C fp64 oracle, OpenMP"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

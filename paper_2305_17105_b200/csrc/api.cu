@@ -16,7 +16,7 @@
 namespace ntc {
 int profile_id(const ntc_desc* d);
 uint32_t decode_wimg_bytes(int pid, int hm);
-int decode_k1(int pid);
+cudaError_t build_wimg(int pid, int hm, const uint16_t* w, int c, uint8_t* img, cudaStream_t s);
 cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cudaStream_t s);
 cudaError_t launch_debug_assemble(int pid, const DecodeParams& p, cudaStream_t s);
 }  // namespace ntc
@@ -189,7 +189,6 @@ struct ntc_material {
     uint4* wimg = nullptr;
     uint32_t wimg_bytes = 0;
     LevelGeom lv[MAX_LEVELS];
-    float b2[HID], b2b[HID], b3[16];
     int num_sms = 148;
 };
 
@@ -206,39 +205,6 @@ __global__ void pack_kernel(const uint8_t* __restrict__ codes, int64_t src_off, 
     }
     uint8_t* o = dst + cell * cell_bytes;
     for (int b = 0; b < cell_bytes; ++b) o[b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
-}
-
-// Weight image: W1 (+b1 column at k = D) in K1/64 SW128 atoms of 64 rows, W2 [, W2b], W3 (16 rows)
-__global__ void wimg_kernel(const uint16_t* __restrict__ w, int D, int K1atoms, int hm, int c, uint8_t* __restrict__ img) {
-    const int n1 = K1atoms * 64 * 64, n2 = 64 * 64, n3 = 16 * 64;
-    const int total = n1 + hm * n2 + n3;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= total) return;
-    const int P1 = D * HID, P2 = HID * HID;
-    uint16_t v = 0;
-    uint32_t off;
-    if (i < n1) {
-        const int atom = i / 4096, r = (i % 4096) / 64, kk = i % 64, k = atom * 64 + kk;
-        if (k < D) v = w[r * D + k];
-        else if (k == D) v = w[P1 + r];
-        off = atom * 8192 + sw128_offset(r, kk);
-    } else if (i < n1 + hm * n2) {
-        const int l = (i - n1) / n2, e = (i - n1) % n2, r = e / 64, k = e % 64;
-        v = w[P1 + HID + l * (P2 + HID) + r * HID + k];
-        off = K1atoms * 8192 + l * 8192 + sw128_offset(r, k);
-    } else {
-        const int e = i - n1 - hm * n2, r = e / 64, k = e % 64;
-        const int base = P1 + HID + hm * (P2 + HID);
-        if (r < c) v = w[base + r * HID + k];
-        off = K1atoms * 8192 + hm * 8192 + sw128_offset(r, k);
-    }
-    *reinterpret_cast<uint16_t*>(img + off) = v;
-}
-
-static float half_bits_to_float(uint16_t h) {
-    __half_raw r;
-    r.x = h;
-    return __half2float(__half(r));
 }
 
 static uint16_t float_to_half_bits(double v) {
@@ -269,6 +235,8 @@ extern "C" ntc_status ntc_material_create(const ntc_desc* d, const uint8_t* code
         ntc_grid_layout(d, j, &r0, &r1, &o0, &o1);
         m->lv[j].r0 = r0;
         m->lv[j].r1 = r1;
+        m->lv[j].lr0 = ilog2i(r0);
+        m->lv[j].lr1 = ilog2i(r1);
         m->lv[j].off0 = bytes;
         bytes += ((int64_t)r0 * r0 * cb0 + 15) / 16 * 16;
         m->lv[j].off1 = bytes;
@@ -295,27 +263,13 @@ extern "C" ntc_status ntc_material_create(const ntc_desc* d, const uint8_t* code
                 codes, src_off[2 * j + k], n, k ? d->c1 : d->c0, k ? d->b1 : d->b0, k ? cb1 : cb0,
                 m->grids + (k ? m->lv[j].off1 : m->lv[j].off0));
         }
-    const int D = 4 * d->c0 + d->c1 + 13;
-    const int k1atoms = (decode_k1(m->pid) + 63) / 64;
-    const int total = k1atoms * 4096 + hm * 4096 + 1024;
-    wimg_kernel<<<(total + 255) / 256, 256, 0, st>>>(weights_f16, D, k1atoms, hm, d->channels,
-                                                      reinterpret_cast<uint8_t*>(m->wimg));
-    // biases of layers 2.. for the epilogues (kernel parameters)
-    const int64_t P = ntc_num_params(d);
-    std::vector<uint16_t> hw(P);
-    e = cudaMemcpyAsync(hw.data(), weights_f16, P * 2, cudaMemcpyDeviceToHost, st);
+    e = build_wimg(m->pid, hm, weights_f16, d->channels, reinterpret_cast<uint8_t*>(m->wimg), st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
         ntc_material_destroy(m);
         return cuda_fail(e, "material upload");
     }
-    const int64_t o2 = (int64_t)D * HID + HID;
-    for (int i = 0; i < HID; ++i) m->b2[i] = half_bits_to_float(hw[o2 + HID * HID + i]);
-    const int64_t o2b = o2 + HID * HID + HID;
-    for (int i = 0; i < HID; ++i) m->b2b[i] = hm == 2 ? half_bits_to_float(hw[o2b + HID * HID + i]) : 0.0f;
-    const int64_t o3 = o2 + hm * (HID * HID + HID) + (int64_t)HID * d->channels;
-    for (int i = 0; i < 16; ++i) m->b3[i] = i < d->channels ? half_bits_to_float(hw[o3 + i]) : 0.0f;
     *out = m;
     return NTC_OK;
 }
@@ -357,9 +311,6 @@ static DecodeParams base_params(const ntc_material* m) {
         for (int k = 0; k < 3; ++k) p.pe_words[q][k] = (uint32_t)v[2 * k] | ((uint32_t)v[2 * k + 1] << 16);
         p.pe_words[q][3] = 0;
     }
-    memcpy(p.b2, m->b2, sizeof p.b2);
-    memcpy(p.b2b, m->b2b, sizeof p.b2b);
-    memcpy(p.b3, m->b3, sizeof p.b3);
     return p;
 }
 
@@ -379,14 +330,14 @@ static ntc_status launch_tiles(const ntc_material* m, int mip_first, int mip_cou
     int64_t t = 0;
     for (int i = 0; i < mip_count; ++i) {
         const int64_t w = m->d.width >> (mip_first + i);
-        p.tile_start[i] = t;
+        p.tile_start[i] = (int32_t)t;
         t += (w * w + TILE_M - 1) / TILE_M;
         p.out_off[i] = out_off[i];
         p.row_stride[i] = row_stride[i];
     }
-    for (int i = mip_count; i <= MAX_MIPS; ++i) p.tile_start[i] = INT64_MAX;
-    p.tile_start[mip_count] = t;
-    p.n_tiles = t;
+    for (int i = mip_count; i <= MAX_MIPS; ++i) p.tile_start[i] = INT32_MAX;
+    p.tile_start[mip_count] = (int32_t)t;
+    p.n_tiles = (int32_t)t;
     cudaError_t e = launch_decode(m->pid, m->d.hidden_mats, p, grid_for(m, t), st);
     return e == cudaSuccess ? NTC_OK : cuda_fail(e, "decode_kernel");
 }

@@ -1,0 +1,282 @@
+// assemble.cuh -- per-texel addressing, latent fetch and fp16 input-row assembly shared by
+// the decode kernels and the debug export (product code).
+//
+// X column order inside the GPU path: the G0 part is permuted so that two codes can be
+// dequantised with one byte-permute + mask + HFMA2 (see g0_word_cols); the W1 image is
+// permuted identically (the MLP is invariant under a joint permutation of X and W1's
+// columns) and ntc_debug_assemble un-permutes to the canonical order of reading R4.
+#pragma once
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace ntc {
+
+// ------------------------------------------------------------------ G0 column permutation
+// word index wi in [0, 2*C0) of the G0 part, lane l in {0,1} -> canonical X column
+// (tap * C0 + channel) of reading R4.
+__host__ __device__ constexpr int g0_word_col(int C0, int B0, int wi, int l) {
+    if (C0 == 8 && B0 == 2) {  // per tap: (k, k+4)
+        return (wi / 4) * 8 + (wi % 4) + 4 * l;
+    }
+    if (C0 == 12 && B0 == 2) {  // per tap (k, k+4) from bytes 0/1; byte 2 paired across taps
+        if (wi < 16) return (wi / 4) * 12 + (wi % 4) + 4 * l;
+        const int j = wi - 16, pi = j / 4, k = j % 4;
+        return (2 * pi + l) * 12 + 8 + k;
+    }
+    if (C0 == 12 && B0 == 4) {  // per tap: (q, q+4) q<4 ; (8+q, 10+q) q<2
+        const int t = wi / 6, k = wi % 6;
+        return t * 12 + (k < 4 ? k + 4 * l : 8 + (k - 4) + 2 * l);
+    }
+    if (C0 == 16 && B0 == 4) {  // per tap: (q, q+4) ; (8+q, 12+q)
+        const int t = wi / 8, k = wi % 8;
+        return t * 16 + (k < 4 ? k + 4 * l : 8 + (k - 4) + 4 * l);
+    }
+    return -1;
+}
+
+// ------------------------------------------------------------------ packed cells
+template <int BYTES>
+struct Cell {
+    uint32_t w[BYTES >= 4 ? BYTES / 4 : 1];
+};
+
+template <int BYTES>
+__device__ __forceinline__ Cell<BYTES> load_cell(const uint8_t* base, int64_t idx) {
+    Cell<BYTES> c;
+    if constexpr (BYTES == 1) {
+        c.w[0] = __ldg(base + idx);
+    } else if constexpr (BYTES == 2) {
+        c.w[0] = __ldg(reinterpret_cast<const uint16_t*>(base) + idx);
+    } else if constexpr (BYTES == 4) {
+        c.w[0] = __ldg(reinterpret_cast<const uint32_t*>(base) + idx);
+    } else if constexpr (BYTES == 8) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(base) + idx);
+        c.w[0] = v.x;
+        c.w[1] = v.y;
+    } else {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(base) + idx);
+        c.w[0] = v.x;
+        c.w[1] = v.y;
+        c.w[2] = v.z;
+        c.w[3] = v.w;
+    }
+    return c;
+}
+
+// dequantise the two codes held in bits [0,B) and [16,16+B) of `lanes` (already masked):
+// half(0x6400 | code) = 1024 + code; one HFMA2 gives (code - N/2 + 1) / N exactly
+// (R10).
+template <int B>
+__device__ __forceinline__ uint32_t dequant2(uint32_t lanes) {
+    constexpr float Q = 1.0f / (float)(1 << B);
+    constexpr float OFF = (float)((1 << B) / 2 - 1);
+    const uint32_t v = lanes | 0x64006400u;
+    __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&v), __float2half2_rn(Q),
+                        __float2half2_rn(-(1024.0f + OFF) * Q));
+    return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// 4-bit codes: split a 32-bit word of `nch` channels into lane pairs (bits 0-3 | 16-19)
+template <int NCH>
+__device__ __forceinline__ void nib_lanes(uint32_t w, uint32_t* out) {
+    if constexpr (NCH == 8) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[q] = (w >> (4 * q)) & 0x000F000Fu;  // (q, q+4)
+    } else if constexpr (NCH == 4) {
+        const uint32_t y = __byte_perm(w, 0u, 0x4140);                     // [b0, 0, b1, 0]
+        out[0] = y & 0x000F000Fu;                                          // (0, 2)
+        out[1] = (y >> 4) & 0x000F000Fu;                                   // (1, 3)
+    } else {
+        const uint32_t y = w | (w << 12);
+        out[0] = y & 0x000F000Fu;                                          // (0, 1)
+    }
+}
+
+// ------------------------------------------------------------------ fetch (a1 + loads)
+template <class P>
+struct Fetch {
+    Cell<P::CELL0> g0[4];
+    Cell<P::CELL1> g1[4];
+    uint32_t wt[4];  // bilinear weights of the G1 taps in units of 1/256 (exact)
+    int m, x, y;
+    bool valid, bad;
+    uint16_t* dst;   // output row of this texel
+};
+
+// R1/R2/R3: u = (x + 1/2) r / w_m - 1/2 with clamp-to-edge taps (i, j), (i+1, j), (i, j+1),
+// (i+1, j+1).  All sizes are powers of two, so in integers: num = (2x + 1) r - w_m,
+// i = floor(num / 2 w_m) (arithmetic shift), frac = (num mod 2 w_m) / 2 w_m.  The G1
+// fractional offsets are multiples of 1/16 (r1 / w_m >= 1/8 for every compiled profile),
+// so the bilinear weights are exact multiples of 1/256.
+template <class P>
+__device__ __forceinline__ void fetch_texel(const DecodeParams& p, int m, int x, int y, Fetch<P>& f,
+                                            int32_t* dbg_addr) {
+    f.m = m;
+    f.x = x;
+    f.y = y;
+    const int j = p.level_of[m];
+    const LevelGeom g = p.lv[j];
+    const int lw = p.M - 1 - m;  // log2(w_m)
+    const int xs = 2 * x + 1, ys = 2 * y + 1;
+    int tx0[2], ty0[2], tx1[2], ty1[2];
+    {
+        const int nx = (xs << g.lr0) - (1 << lw), ny = (ys << g.lr0) - (1 << lw);
+        const int i = nx >> (lw + 1), k = ny >> (lw + 1);
+        tx0[0] = max(i, 0);
+        tx0[1] = min(i + 1, g.r0 - 1);
+        ty0[0] = max(k, 0);
+        ty0[1] = min(k + 1, g.r0 - 1);
+    }
+    {
+        const int nx = (xs << g.lr1) - (1 << lw), ny = (ys << g.lr1) - (1 << lw);
+        const int i = nx >> (lw + 1), k = ny >> (lw + 1);
+        const int mask = (2 << lw) - 1;
+        const uint32_t ax = (uint32_t)(((nx & mask) << 4) >> (lw + 1));
+        const uint32_t ay = (uint32_t)(((ny & mask) << 4) >> (lw + 1));
+        f.wt[0] = (16u - ax) * (16u - ay);
+        f.wt[1] = ax * (16u - ay);
+        f.wt[2] = (16u - ax) * ay;
+        f.wt[3] = ax * ay;
+        tx1[0] = max(i, 0);
+        tx1[1] = min(i + 1, g.r1 - 1);
+        ty1[0] = max(k, 0);
+        ty1[1] = min(k + 1, g.r1 - 1);
+    }
+    const uint8_t* g0 = p.grids + g.off0;
+    const uint8_t* g1 = p.grids + g.off1;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        f.g0[t] = load_cell<P::CELL0>(g0, (uint32_t)(ty0[t >> 1] * g.r0 + tx0[t & 1]));
+        f.g1[t] = load_cell<P::CELL1>(g1, (uint32_t)(ty1[t >> 1] * g.r1 + tx1[t & 1]));
+    }
+    if (dbg_addr) {
+        dbg_addr[0] = j;
+        for (int t = 0; t < 4; ++t) {
+            dbg_addr[1 + 2 * t] = tx0[t & 1];
+            dbg_addr[2 + 2 * t] = ty0[t >> 1];
+            dbg_addr[9 + 2 * t] = tx1[t & 1];
+            dbg_addr[10 + 2 * t] = ty1[t >> 1];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ assembly (a2-a4)
+// X = [G0 taps (permuted pairs) | bilinear G1 | PE_x(6) | PE_y(6) | LOD | 1 | 0 ...] as
+// K1W half2 words; the trailing 1 multiplies the b1 column of the W1 image.
+template <class P>
+__device__ __forceinline__ void assemble_words(const DecodeParams& p, const uint32_t* s_pe, const Fetch<P>& f,
+                                               uint32_t (&w)[P::K1W]) {
+    // ---- G0: four unfiltered taps (learned interpolation)
+    if constexpr (P::C0 == 8 && P::B0 == 2) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t y = __byte_perm(f.g0[t].w[0], 0u, 0x4140);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[4 * t + k] = dequant2<2>((y >> (2 * k)) & 0x00030003u);
+        }
+    } else if constexpr (P::C0 == 12 && P::B0 == 2) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t y = __byte_perm(f.g0[t].w[0], 0u, 0x4140);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[4 * t + k] = dequant2<2>((y >> (2 * k)) & 0x00030003u);
+        }
+#pragma unroll
+        for (int pi = 0; pi < 2; ++pi) {
+            const uint32_t y = __byte_perm(f.g0[2 * pi].w[0], f.g0[2 * pi + 1].w[0], 0x7672);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[16 + 4 * pi + k] = dequant2<2>((y >> (2 * k)) & 0x00030003u);
+        }
+    } else if constexpr (P::C0 == 12 && P::B0 == 4) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            uint32_t l[6];
+            nib_lanes<8>(f.g0[t].w[0], l);
+            nib_lanes<4>(f.g0[t].w[1], l + 4);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) w[6 * t + k] = dequant2<4>(l[k]);
+        }
+    } else {
+        static_assert(P::C0 == 16 && P::B0 == 4, "unsupported G0 profile");
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            uint32_t l[8];
+            nib_lanes<8>(f.g0[t].w[0], l);
+            nib_lanes<8>(f.g0[t].w[1], l + 4);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w[8 * t + k] = dequant2<4>(l[k]);
+        }
+    }
+    // ---- G1: bilinear as integer multiply-adds on two 16-bit lanes:
+    // S = sum_t wt_t * code_t (< 2^16), value = (S - 256 (N/2-1)) / (256 N), exact in fp32,
+    // rounded once to fp16.
+    static_assert(P::B1 == 4, "G1 path assumes 4-bit codes (all Table 2 profiles)");
+    {
+        constexpr int NL = P::C1 / 2;
+        uint32_t S[NL];
+        float v[P::C1];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            uint32_t l[NL];
+            int cb[NL];  // first channel of each lane pair, second = cb + step
+            int st[NL];
+            int n = 0;
+#pragma unroll
+            for (int wd = 0; wd * 8 < P::C1; ++wd) {
+                const int nch = P::C1 - wd * 8 >= 8 ? 8 : P::C1 - wd * 8;
+                if (nch == 8) {
+                    nib_lanes<8>(f.g1[t].w[wd], l + n);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 4; }
+                    n += 4;
+                } else if (nch == 4) {
+                    nib_lanes<4>(f.g1[t].w[wd], l + n);
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 2; }
+                    n += 2;
+                } else {
+                    nib_lanes<2>(f.g1[t].w[wd], l + n);
+                    cb[n] = wd * 8;
+                    st[n] = 1;
+                    n += 1;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NL; ++i) S[i] = t == 0 ? l[i] * f.wt[0] : S[i] + l[i] * f.wt[t];
+            if (t == 3) {
+                constexpr float SC = 1.0f / (256.0f * 16.0f);
+                constexpr float BI = -(8388608.0f + 256.0f * 7.0f) / (256.0f * 16.0f);
+#pragma unroll
+                for (int i = 0; i < NL; ++i) {
+                    v[cb[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7610)), SC, BI);
+                    v[cb[i] + st[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7632)), SC, BI);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < P::C1 / 2; ++k) w[2 * P::C0 + k] = pack_half2(v[2 * k], v[2 * k + 1]);
+    }
+    // ---- PE from the per-axis table, then LOD + bias one
+    constexpr int PEW = (4 * P::C0 + P::C1) / 2;
+    const uint4 px = *reinterpret_cast<const uint4*>(s_pe + 4 * (f.x & 7));
+    const uint4 py = *reinterpret_cast<const uint4*>(s_pe + 4 * (f.y & 7));
+    w[PEW + 0] = px.x;
+    w[PEW + 1] = px.y;
+    w[PEW + 2] = px.z;
+    w[PEW + 3] = py.x;
+    w[PEW + 4] = py.y;
+    w[PEW + 5] = py.z;
+    w[PEW + 6] = p.lod_word[f.m];
+#pragma unroll
+    for (int k = PEW + 7; k < P::K1W; ++k) w[k] = 0u;
+}
+
+// canonical (R4) column of GPU X column `col`
+template <class P>
+__host__ __device__ constexpr int canonical_col(int col) {
+    return col < 4 * P::C0 ? g0_word_col(P::C0, P::B0, col / 2, col & 1) : col;
+}
+
+}  // namespace ntc

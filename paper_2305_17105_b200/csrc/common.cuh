@@ -33,6 +33,7 @@ struct Prof {
 // Per-level geometry for the device: resolutions and byte offsets into the packed grids.
 struct LevelGeom {
     int32_t r0, r1;
+    int32_t lr0, lr1;    // log2 of r0, r1
     int64_t off0, off1;  // byte offsets of packed G0 / G1 of this level
 };
 
@@ -49,10 +50,10 @@ struct DecodeParams {
     uint32_t pe_words[8][4];      // PE of one axis at p = x mod 8, as 3 half2 words (+pad)
     // mode 0
     int32_t mip_first, mip_count;
-    int64_t tile_start[MAX_MIPS + 1];
+    int32_t tile_start[MAX_MIPS + 1];
     int64_t out_off[MAX_MIPS];     // element offset of mip in out
     int64_t row_stride[MAX_MIPS];  // elements
-    int64_t n_tiles;
+    int32_t n_tiles;
     // mode 1 / 2
     const ntc_query* q;
     int64_t nq;
@@ -60,9 +61,6 @@ struct DecodeParams {
     int32_t* dbg_addr;
     uint16_t* dbg_X;
     uint16_t* out;
-    float b2[HID];
-    float b2b[HID];
-    float b3[16];
 };
 
 }  // namespace ntc

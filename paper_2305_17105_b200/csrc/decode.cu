@@ -1,178 +1,25 @@
 // decode.cu -- per-texel NTC decode on sm_100a (tcgen05 + TMEM), product code.
 //
-// One persistent CTA per SM, NWG = 4 warpgroups.  Each warpgroup owns a pipeline of
-// 128-texel tiles (TMEM lane r <-> texel r <-> thread r of the warpgroup):
-//   a1-a4  every thread assembles its texel's fp16 input row X (G0 2x2 gather, G1 bilinear,
-//          PE, LOD, constant 1 for the folded bias b1) and stores it into a K-major,
-//          128B-swizzled SMEM tile;
-//   a5     one elected thread issues tcgen05.mma  D1[tmem] = X * W1^T  (M=128, N=64);
-//   a5/a6  tcgen05.ld D1 -> +b, hardGELU -> fp16 -> SMEM (A operand of the next layer);
-//   a7     D3 = H2 * W3^T (N=16) -> +b3, clamp [0,1] -> fp16 -> global (y, x, ch).
+// One persistent CTA per SM, 4 warpgroups (2 for profiles with K1 > 64).  Each warpgroup
+// ping-pongs between two 128-texel tile contexts (TMEM lane r <-> texel r <-> thread r of
+// the warpgroup), so the tensor core works on one context while the threads run the
+// other's epilogue:
+//   a1     every thread resolves its texel of the NEXT tile and issues its 8 latent-cell
+//          loads, which stay in flight while the current tile runs through the MLP;
+//   a2-a4  it assembles its fp16 input row X (G0 2x2 gather, G1 bilinear, PE, LOD, a
+//          constant 1 for the folded bias b1) into a K-major, 128B-swizzled SMEM tile;
+//   a5-a7  one elected thread issues tcgen05.mma per layer (M=128; N=64, 64, 16); the
+//          biases of layers 2/3 enter as one extra K=16 MMA against a constant ones tile;
+//          the epilogue is tcgen05.ld -> hardGELU (FFMA.SAT + packed FMUL2) -> fp16 ->
+//          SMEM A operand of the next layer; the output is clamped to [0,1] and stored.
 // The whole MLP weight set lives in SMEM for the CTA's lifetime (one copy per SM).
 #include <cuda_fp16.h>
 
+#include "assemble.cuh"
 #include "common.cuh"
 #include "ptx.cuh"
 
 namespace ntc {
-
-// ------------------------------------------------------------------ addressing (a1)
-// R1/R2/R3: u = (x + 1/2) r / w_m - 1/2 (exact in fp32: r / w_m is a power of two),
-// taps (i, j), (i+1, j), (i, j+1), (i+1, j+1) clamped to the grid.
-struct Taps {
-    int32_t j;
-    int32_t x0[2], y0[2];  // G0 tap columns / rows
-    int32_t x1[2], y1[2];  // G1 tap columns / rows
-    float fx, fy;          // G1 fractional offsets (dyadic, exact)
-};
-
-__device__ __forceinline__ void address(const DecodeParams& p, int m, int x, int y, Taps& t) {
-    const int j = p.level_of[m];
-    const int r0 = p.lv[j].r0, r1 = p.lv[j].r1;
-    const float wm = (float)(p.W >> m);
-    t.j = j;
-    {
-        const float s = (float)r0 / wm;
-        const float u = ((float)x + 0.5f) * s - 0.5f, v = ((float)y + 0.5f) * s - 0.5f;
-        const int i = (int)floorf(u), k = (int)floorf(v);
-        t.x0[0] = min(max(i, 0), r0 - 1);
-        t.x0[1] = min(max(i + 1, 0), r0 - 1);
-        t.y0[0] = min(max(k, 0), r0 - 1);
-        t.y0[1] = min(max(k + 1, 0), r0 - 1);
-    }
-    {
-        const float s = (float)r1 / wm;
-        const float u = ((float)x + 0.5f) * s - 0.5f, v = ((float)y + 0.5f) * s - 0.5f;
-        const float fu = floorf(u), fv = floorf(v);
-        const int i = (int)fu, k = (int)fv;
-        t.fx = u - fu;
-        t.fy = v - fv;
-        t.x1[0] = min(max(i, 0), r1 - 1);
-        t.x1[1] = min(max(i + 1, 0), r1 - 1);
-        t.y1[0] = min(max(k, 0), r1 - 1);
-        t.y1[1] = min(max(k + 1, 0), r1 - 1);
-    }
-}
-
-// ------------------------------------------------------------------ packed cells
-template <int BYTES>
-struct Cell {
-    uint32_t w[BYTES >= 4 ? BYTES / 4 : 1];
-};
-
-template <int BYTES>
-__device__ __forceinline__ Cell<BYTES> load_cell(const uint8_t* base, int64_t idx) {
-    Cell<BYTES> c;
-    if constexpr (BYTES == 1) {
-        c.w[0] = __ldg(base + idx);
-    } else if constexpr (BYTES == 2) {
-        c.w[0] = __ldg(reinterpret_cast<const uint16_t*>(base) + idx);
-    } else if constexpr (BYTES == 4) {
-        c.w[0] = __ldg(reinterpret_cast<const uint32_t*>(base) + idx);
-    } else if constexpr (BYTES == 8) {
-        uint2 v = __ldg(reinterpret_cast<const uint2*>(base) + idx);
-        c.w[0] = v.x;
-        c.w[1] = v.y;
-    } else {
-        uint4 v = __ldg(reinterpret_cast<const uint4*>(base) + idx);
-        c.w[0] = v.x;
-        c.w[1] = v.y;
-        c.w[2] = v.z;
-        c.w[3] = v.w;
-    }
-    return c;
-}
-
-template <int B, int BYTES>
-__device__ __forceinline__ uint32_t code_of(const Cell<BYTES>& c, int ch) {
-    const int bit = ch * B;
-    return (c.w[bit >> 5] >> (bit & 31)) & ((1u << B) - 1u);
-}
-
-// dequantise two codes to a half2 (idx * Q, idx = code - (N/2 - 1)):
-// half(0x6400 | code) = 1024 + code; one HFMA2 maps it to (code - N/2 + 1) / N exactly.
-template <int B>
-__device__ __forceinline__ uint32_t dequant_pair(uint32_t lo, uint32_t hi) {
-    constexpr float Q = 1.0f / (float)(1 << B);
-    constexpr float OFF = (float)((1 << B) / 2 - 1);
-    const uint32_t v = lo | (hi << 16) | 0x64006400u;
-    const __half2 s = __float2half2_rn(Q);
-    const __half2 o = __float2half2_rn(-(1024.0f + OFF) * Q);
-    __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&v), s, o);
-    return *reinterpret_cast<uint32_t*>(&r);
-}
-
-__device__ __forceinline__ float code_f32(uint32_t code) {
-    return __uint_as_float(0x4B000000u | code) - 8388608.0f;  // exact integer -> float
-}
-
-// ------------------------------------------------------------------ input assembly (a2-a4)
-// X = [G0 taps (tap-major, channel-minor) | bilinear G1 | PE_x(6) | PE_y(6) | LOD | 1 | 0...]
-// as K1W half2 words (R4; the trailing 1 multiplies the b1 column of the W1 image).
-template <class P>
-__device__ __forceinline__ void assemble_row(const DecodeParams& p, const uint32_t* s_pe, int m, int x, int y,
-                                             uint32_t (&w)[P::K1W], int32_t* dbg_addr) {
-    Taps t;
-    address(p, m, x, y, t);
-    const LevelGeom g = p.lv[t.j];
-    const uint8_t* g0 = p.grids + g.off0;
-    const uint8_t* g1 = p.grids + g.off1;
-    // G0: four unfiltered taps ("learned interpolation")
-#pragma unroll
-    for (int tp = 0; tp < 4; ++tp) {
-        const int cx = t.x0[tp & 1], cy = t.y0[tp >> 1];
-        const Cell<P::CELL0> c = load_cell<P::CELL0>(g0, (int64_t)cy * g.r0 + cx);
-#pragma unroll
-        for (int k = 0; k < P::C0 / 2; ++k)
-            w[tp * (P::C0 / 2) + k] = dequant_pair<P::B0>(code_of<P::B0>(c, 2 * k), code_of<P::B0>(c, 2 * k + 1));
-    }
-    // G1: bilinear; sums of dyadic products, exact in fp32, rounded once
-    {
-        Cell<P::CELL1> c[4];
-#pragma unroll
-        for (int tp = 0; tp < 4; ++tp)
-            c[tp] = load_cell<P::CELL1>(g1, (int64_t)t.y1[tp >> 1] * g.r1 + t.x1[tp & 1]);
-        const float wt[4] = {(1.0f - t.fx) * (1.0f - t.fy), t.fx * (1.0f - t.fy), (1.0f - t.fx) * t.fy,
-                             t.fx * t.fy};
-        constexpr float Q = 1.0f / (float)(1 << P::B1);
-        constexpr float OFFQ = (float)((1 << P::B1) / 2 - 1) / (float)(1 << P::B1);
-#pragma unroll
-        for (int k = 0; k < P::C1 / 2; ++k) {
-            float v[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                float a = wt[0] * code_f32(code_of<P::B1>(c[0], 2 * k + e));
-                a = fmaf(wt[1], code_f32(code_of<P::B1>(c[1], 2 * k + e)), a);
-                a = fmaf(wt[2], code_f32(code_of<P::B1>(c[2], 2 * k + e)), a);
-                a = fmaf(wt[3], code_f32(code_of<P::B1>(c[3], 2 * k + e)), a);
-                v[e] = fmaf(a, Q, -OFFQ);
-            }
-            w[2 * P::C0 + k] = pack_half2(v[0], v[1]);
-        }
-    }
-    // PE from the 8-entry per-axis table, LOD + bias one
-    constexpr int PEW = (4 * P::C0 + P::C1) / 2;
-    const uint4 px = *reinterpret_cast<const uint4*>(s_pe + 4 * (x & 7));
-    const uint4 py = *reinterpret_cast<const uint4*>(s_pe + 4 * (y & 7));
-    w[PEW + 0] = px.x;
-    w[PEW + 1] = px.y;
-    w[PEW + 2] = px.z;
-    w[PEW + 3] = py.x;
-    w[PEW + 4] = py.y;
-    w[PEW + 5] = py.z;
-    w[PEW + 6] = p.lod_word[m];
-#pragma unroll
-    for (int k = PEW + 7; k < P::K1W; ++k) w[k] = 0u;
-    if (dbg_addr) {
-        dbg_addr[0] = t.j;
-        for (int tp = 0; tp < 4; ++tp) {
-            dbg_addr[1 + 2 * tp] = t.x0[tp & 1];
-            dbg_addr[2 + 2 * tp] = t.y0[tp >> 1];
-            dbg_addr[9 + 2 * tp] = t.x1[tp & 1];
-            dbg_addr[10 + 2 * tp] = t.y1[tp >> 1];
-        }
-    }
-}
 
 // store NW half2 words of row `row` into a K-major SW128 tile of 128 rows
 template <int NW>
@@ -185,61 +32,149 @@ __device__ __forceinline__ void store_row(uint32_t tile, int row, const uint32_t
     }
 }
 
-// hardGELU = z * sat(z/3 + 1/2)
-__device__ __forceinline__ float hardgelu(float z) { return z * __saturatef(fmaf(z, 1.0f / 3.0f, 0.5f)); }
+// hardGELU of a column pair: z * sat(z/3 + 1/2), packed fp32 multiply
+__device__ __forceinline__ uint32_t hardgelu2(uint32_t a, uint32_t b) {
+    const float2 z = make_float2(__uint_as_float(a), __uint_as_float(b));
+    const float2 t = make_float2(__saturatef(fmaf(z.x, 1.0f / 3.0f, 0.5f)), __saturatef(fmaf(z.y, 1.0f / 3.0f, 0.5f)));
+    const float2 h = __fmul2_rn(z, t);
+    return pack_half2(h.x, h.y);
+}
 
-// TMEM accumulator columns [0, 64) of this thread's lane -> +bias -> hardGELU -> 32 half2
-template <int LAYER>
-__device__ __forceinline__ void epilogue_hidden(const DecodeParams& p, uint32_t taddr, uint32_t (&h)[32]) {
+// TMEM accumulator columns [0, 64) of this thread's lane (bias already accumulated)
+// -> hardGELU -> fp16 -> row `row` of the SW128 A tile, 32 columns at a time
+__device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, int row) {
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         uint32_t r[32];
         tmem_ld32(taddr + 32 * half, r);
         tmem_wait_ld();
+        uint32_t h[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
-            if constexpr (LAYER == 2) {
-                z0 += p.b2[32 * half + 2 * i];
-                z1 += p.b2[32 * half + 2 * i + 1];
-            } else if constexpr (LAYER == 3) {
-                z0 += p.b2b[32 * half + 2 * i];
-                z1 += p.b2b[32 * half + 2 * i + 1];
-            }
-            h[16 * half + i] = pack_half2(hardgelu(z0), hardgelu(z1));
+        for (int i = 0; i < 16; ++i) h[i] = hardgelu2(r[2 * i], r[2 * i + 1]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int chunk = 4 * half + c;
+            sts128(tile + (uint32_t)row * 128u + ((uint32_t)(chunk ^ (row & 7)) << 4), h[4 * c], h[4 * c + 1],
+                   h[4 * c + 2], h[4 * c + 3]);
         }
     }
 }
 
 template <class P, int HM>
 struct DecodeSmem {
+    static constexpr int NWG = P::K1_ATOMS == 1 ? 4 : 2;  // warpgroups per CTA
     static constexpr uint32_t W1_BYTES = P::K1_ATOMS * 64 * 128;
-    static constexpr uint32_t W2_BYTES = 64 * 128;
-    static constexpr uint32_t W3_BYTES = 16 * 128;
+    static constexpr uint32_t W2_BYTES = 2 * 64 * 128;  // weights atom + bias atom
+    static constexpr uint32_t W3_BYTES = 2 * 16 * 128;
     static constexpr uint32_t WIMG = W1_BYTES + HM * W2_BYTES + W3_BYTES;
-    static constexpr uint32_t ABUF = P::K1_ATOMS * 128 * 128;
-    static constexpr uint32_t BYTES = 1024 /*align slack*/ + WIMG + NWG * ABUF + 128 /*pe*/ + 64 /*bars*/ + 16;
+    static constexpr uint32_t ONES = 128 * 128;         // constant A tile: column 0 = 1
+    static constexpr uint32_t ABUF = P::K1_ATOMS * 128 * 128;  // one per tile context
+    static constexpr uint32_t BYTES = 1024 + WIMG + ONES + NWG * 2 * ABUF + 128 /*pe*/ + 128 /*bars*/ + 16;
+};
+
+// resolve the texel of row `row` of `tile`, its output address, and issue its latent loads
+template <class P>
+__device__ __forceinline__ void fetch_tile(const DecodeParams& p, int tile, int row, Fetch<P>& f) {
+    int m = 0, x = 0, y = 0;
+    bool valid, bad = false;
+    if (p.mode == 0) {
+        int mi = 0;
+        while (tile >= p.tile_start[mi + 1]) ++mi;
+        m = p.mip_first + mi;
+        const int local = (tile - p.tile_start[mi]) * TILE_M + row;
+        const int lw = p.M - 1 - m;  // log2(w_m)
+        valid = local < (1 << (2 * lw));
+        if (valid) {
+            x = local & ((1 << lw) - 1);
+            y = local >> lw;
+        }
+        f.dst = p.out + (p.out_off[mi] + (int64_t)y * p.row_stride[mi] + x * p.c);
+    } else {
+        const int64_t qi = (int64_t)tile * TILE_M + row;
+        valid = qi < p.nq;
+        if (valid) {
+            const uint2 qq = __ldg(reinterpret_cast<const uint2*>(p.q) + qi);
+            x = (int)(qq.x & 0xFFFFu);
+            y = (int)(qq.x >> 16);
+            m = (int)(qq.y & 0xFFu);
+            if (m >= p.M || x >= (p.W >> m) || y >= (p.W >> m)) {
+                bad = true;
+                m = p.M - 1;
+                x = y = 0;
+            }
+        }
+        f.dst = p.out + qi * p.c;
+    }
+    f.valid = valid;
+    f.bad = bad;
+    fetch_texel<P>(p, m, x, y, f, nullptr);
+}
+
+// a7 store of one texel's c fp16 channels (o = 8 packed pairs).  c is uniform, so the
+// branches below are uniform: even c -> every texel row is 4-byte aligned (b32 pairs),
+// odd c -> b16 stores.
+__device__ __forceinline__ void store_output(const DecodeParams& p, uint16_t* dst, bool valid, bool bad,
+                                             const uint32_t (&o)[8]) {
+    if (!valid) return;
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = bad ? 0x7E007E00u : o[k];  // NaN row for a bad query
+    if (bad && p.status) atomicOr(p.status, (int)NTC_ERR_OUT_OF_RANGE);
+    const int c = p.c;
+    if ((c & 1) == 0) {
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (2 * k < c) d32[k] = v[k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (2 * k < c) dst[2 * k] = (uint16_t)(v[k] & 0xFFFFu);
+            if (2 * k + 1 < c) dst[2 * k + 1] = (uint16_t)(v[k] >> 16);
+        }
+    }
+}
+
+// Per-warpgroup ping-pong over two tile contexts: while the tensor core runs one
+// context's layer, the warpgroup's threads run the other context's epilogue.
+template <class P>
+struct Ctx {
+    int tile;           // current tile of this context (>= ntiles: idle)
+    Fetch<P> nxt;       // prefetched latents of the context's next tile
+    uint16_t* dst;      // current texel's output row
+    bool valid, bad;
+    uint32_t phase;
+    uint32_t abuf, tcol;
+    uint64_t* bar;
+    int id;             // context index (named barrier selector)
+    uint64_t adesc;     // SW128 K-major descriptor of abuf
 };
 
 template <class P, int HM>
-__global__ void __launch_bounds__(NWG * 128, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
+__global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
     using S = DecodeSmem<P, HM>;
+    constexpr int NW = S::NWG;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* s_w = smem;
-    uint8_t* s_a = smem + S::WIMG;
-    uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_a + NWG * S::ABUF);
+    uint8_t* s_ones = smem + S::WIMG;
+    uint8_t* s_a = s_ones + S::ONES;
+    uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_a + NW * 2 * S::ABUF);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_pe + 32);
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + NWG);
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * NW);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wg = warp >> 2, q = warp & 3, row = q * 32 + lane;
 
-    for (uint32_t i = tid; i < S::WIMG / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(s_w)[i] = p.wimg[i];
+    for (uint32_t i = tid; i < S::WIMG / 16; i += blockDim.x) reinterpret_cast<uint4*>(s_w)[i] = p.wimg[i];
+    for (uint32_t i = tid; i < S::ONES / 16; i += blockDim.x) {
+        const uint32_t r = i >> 3, chunk = i & 7;  // 16-byte chunk `chunk` of row r
+        const bool one = chunk == (r & 7);          // logical chunk 0 lands at physical r&7
+        reinterpret_cast<uint4*>(s_ones)[i] = make_uint4(one ? 0x3C00u : 0u, 0u, 0u, 0u);
+    }
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
     if (tid == 0) {
-        for (int i = 0; i < NWG; ++i) mbar_init(&s_bar[i], 1);
+        for (int i = 0; i < 2 * NW; ++i) mbar_init(&s_bar[i], 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -252,134 +187,114 @@ __global__ void __launch_bounds__(NWG * 128, 1) decode_kernel(const __grid_const
     tc_fence_after();
 
     const uint32_t tmem = *s_tmem;
-    const uint32_t t_d = tmem + (uint32_t)wg * 128u;             // this warpgroup's columns
-    const uint32_t t_row = t_d + ((uint32_t)(q * 32) << 16);      // this warp's lane quarter
-    const uint32_t a_tile = smem_u32(s_a + wg * S::ABUF);
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;   // this warp's TMEM lane quarter
     const uint32_t w1 = smem_u32(s_w), w2 = w1 + S::W1_BYTES, w3 = w2 + HM * S::W2_BYTES;
+    // descriptors advance by (bytes >> 4) in their low 14-bit start-address field
+    const uint64_t d_w1 = umma_desc_k_sw128(w1), d_w2 = umma_desc_k_sw128(w2), d_w3 = umma_desc_k_sw128(w3);
+    const uint64_t d_ones = umma_desc_k_sw128(smem_u32(s_ones));
     const bool issuer = (q == 0) && (lane == 0);
+    // Operand hand-off to the MMA issuer: warps 1-3 of the warpgroup only arrive on the
+    // context's named barrier (bar.arrive) and move on to the other context; warp 0 waits
+    // (bar.sync) and issues.  One barrier id per context keeps successive phases apart.
+    auto handoff = [&](int c) {
+        if (q == 0)
+            named_bar_sync(1 + wg * 2 + c, 128);
+        else
+            named_bar_arrive(1 + wg * 2 + c, 128);
+    };
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
-    uint32_t phase = 0;
+    const int ntiles = p.mode == 0 ? p.n_tiles : (int)((p.nq + TILE_M - 1) / TILE_M);
+    const int stride = (int)gridDim.x * NW * 2;  // tiles advance by 2 contexts per warpgroup
 
-    const int64_t ntiles = p.mode == 0 ? p.n_tiles : (p.nq + TILE_M - 1) / TILE_M;
-    for (int64_t tile = (int64_t)blockIdx.x * NWG + wg; tile < ntiles; tile += (int64_t)gridDim.x * NWG) {
-        // ---- resolve this thread's texel
-        int m, x, y;
-        bool valid, bad = false;
-        uint16_t* dst;
-        if (p.mode == 0) {
-            int mi = 0;
-            while (tile >= p.tile_start[mi + 1]) ++mi;
-            m = p.mip_first + mi;
-            const int64_t local = (tile - p.tile_start[mi]) * TILE_M + row;
-            const int lw = p.M - 1 - m;  // log2(w_m)
-            valid = local < ((int64_t)1 << (2 * lw));
-            x = (int)(local & ((1 << lw) - 1));
-            y = (int)(local >> lw);
-            if (!valid) x = y = 0;
-            dst = p.out + p.out_off[mi] + (int64_t)y * p.row_stride[mi] + (int64_t)x * p.c;
-        } else {
-            const int64_t qi = tile * TILE_M + row;
-            valid = qi < p.nq;
-            m = 0;
-            x = y = 0;
-            if (valid) {
-                const uint2 qq = __ldg(reinterpret_cast<const uint2*>(p.q) + qi);
-                x = (int)(qq.x & 0xFFFFu);
-                y = (int)(qq.x >> 16);
-                m = (int)(qq.y & 0xFFu);
-                if (m >= p.M || x >= (p.W >> m) || y >= (p.W >> m)) {
-                    bad = true;
-                    m = p.M - 1;
-                    x = y = 0;
-                }
-            }
-            dst = p.out + qi * p.c;
-        }
-        // ---- a1-a4: assemble X into the swizzled A tile
+    Ctx<P> cx[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        cx[c].tile = ((int)blockIdx.x * NW + wg) * 2 + c;
+        cx[c].phase = 0;
+        cx[c].abuf = smem_u32(s_a + (wg * 2 + c) * S::ABUF);
+        cx[c].tcol = tmem + (uint32_t)(wg * 128 + c * 64);
+        cx[c].bar = &s_bar[wg * 2 + c];
+        cx[c].id = c;
+        cx[c].adesc = umma_desc_k_sw128(cx[c].abuf);
+        if (cx[c].tile < ntiles) fetch_tile<P>(p, cx[c].tile, row, cx[c].nxt);
+    }
+
+    // P0: assemble X of the context's tile from its prefetched latents, MMA1, prefetch next
+    auto phase0 = [&](Ctx<P>& C) {
+        if (C.tile >= ntiles) return;
         {
             uint32_t xw[P::K1W];
-            assemble_row<P>(p, s_pe, m, x, y, xw, nullptr);
-            store_row<P::K1W>(a_tile, row, xw);
+            assemble_words<P>(p, s_pe, C.nxt, xw);
+            store_row<P::K1W>(C.abuf, row, xw);
         }
+        C.dst = C.nxt.dst;
+        C.valid = C.nxt.valid;
+        C.bad = C.nxt.bad;
         fence_proxy_async_smem();
         tc_fence_before();
-        named_bar_sync(1 + wg, 128);
-        // ---- a5: D = X * W1^T (b1 folded through the constant-1 column)
+        handoff(C.id);
         if (issuer) {
             tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < P::K1 / 16; ++k) {
-                const uint64_t ad = umma_desc_k_sw128(a_tile + (k >> 2) * (128 * 128) + (k & 3) * 32);
-                const uint64_t bd = umma_desc_k_sw128(w1 + (k >> 2) * (64 * 128) + (k & 3) * 32);
-                mma_f16_ss(t_d, ad, bd, ID64, k > 0);
-            }
-            mma_commit(&s_bar[wg]);
+            for (int k = 0; k < P::K1 / 16; ++k)
+                mma_f16_ss(C.tcol, C.adesc + (uint64_t)(((k >> 2) * (128 * 128) + (k & 3) * 32) >> 4),
+                           d_w1 + (uint64_t)(((k >> 2) * (64 * 128) + (k & 3) * 32) >> 4), ID64, k > 0);
+            mma_commit(C.bar);
         }
-        mbar_wait(&s_bar[wg], phase);
-        phase ^= 1;
+        const int nt = C.tile + stride;
+        if (nt < ntiles) fetch_tile<P>(p, nt, row, C.nxt);  // loads overlap the MLP
+    };
+    // P1..P(HM+1): wait for the previous MMA, epilogue to the A tile, next layer's MMA
+    auto phase_hidden = [&](Ctx<P>& C, int layer) {
+        if (C.tile >= ntiles) return;
+        mbar_wait(C.bar, C.phase);
+        C.phase ^= 1;
         tc_fence_after();
-        // ---- hidden layers
-#pragma unroll
-        for (int layer = 1; layer <= HM; ++layer) {
-            uint32_t h[32];
-            if (layer == 1)
-                epilogue_hidden<1>(p, t_row, h);
-            else
-                epilogue_hidden<2>(p, t_row, h);
-            store_row<32>(a_tile, row, h);
-            fence_proxy_async_smem();
-            tc_fence_before();
-            named_bar_sync(1 + wg, 128);
-            if (issuer) {
-                tc_fence_after();
-                const uint32_t wl = w2 + (layer - 1) * S::W2_BYTES;
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    mma_f16_ss(t_d, umma_desc_k_sw128(a_tile + k * 32), umma_desc_k_sw128(wl + k * 32), ID64, k > 0);
-                mma_commit(&s_bar[wg]);
-            }
-            mbar_wait(&s_bar[wg], phase);
-            phase ^= 1;
-            tc_fence_after();
-        }
-        {
-            uint32_t h[32];
-            if (HM == 1)
-                epilogue_hidden<2>(p, t_row, h);
-            else
-                epilogue_hidden<3>(p, t_row, h);
-            store_row<32>(a_tile, row, h);
-        }
+        epilogue_hidden(C.tcol + lane_off, C.abuf, row);
         fence_proxy_async_smem();
         tc_fence_before();
-        named_bar_sync(1 + wg, 128);
-        // ---- a7: Y = H * W3^T (N = 16) into columns [64, 80)
+        handoff(C.id);
         if (issuer) {
             tc_fence_after();
+            const bool last = layer == HM;
+            const uint64_t dl = last ? d_w3 : d_w2 + (uint64_t)((layer * S::W2_BYTES) >> 4);
+            const uint64_t bias_atom = last ? (16 * 128) >> 4 : (64 * 128) >> 4;
+            const uint32_t id = last ? ID16 : ID64;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                mma_f16_ss(t_d + 64, umma_desc_k_sw128(a_tile + k * 32), umma_desc_k_sw128(w3 + k * 32), ID16, k > 0);
-            mma_commit(&s_bar[wg]);
+            for (int k = 0; k < 4; ++k) mma_f16_ss(C.tcol, C.adesc + 2 * k, dl + 2 * k, id, k > 0);
+            mma_f16_ss(C.tcol, d_ones, dl + bias_atom, id, 1);
+            mma_commit(C.bar);
         }
-        mbar_wait(&s_bar[wg], phase);
-        phase ^= 1;
+    };
+    // P(HM+2): wait for the output MMA, clamp, store, then start the context's next tile
+    auto phase_out = [&](Ctx<P>& C) {
+        if (C.tile >= ntiles) return;
+        mbar_wait(C.bar, C.phase);
+        C.phase ^= 1;
         tc_fence_after();
-        {
-            uint32_t r[16];
-            tmem_ld16(t_row + 64, r);
-            tmem_wait_ld();
-            if (valid) {
+        uint32_t r[16];
+        tmem_ld16(C.tcol + lane_off, r);
+        tmem_wait_ld();
+        uint32_t o[8];
 #pragma unroll
-                for (int ch = 0; ch < 16; ++ch) {
-                    if (ch < p.c) {
-                        const float v = __saturatef(__uint_as_float(r[ch]) + p.b3[ch]);  // R13
-                        dst[ch] = bad ? (uint16_t)0x7E00u : __half_as_ushort(__float2half_rn(v));
-                    }
-                }
-                if (bad && p.status) atomicOr(p.status, (int)NTC_ERR_OUT_OF_RANGE);
-            }
-        }
+        for (int k = 0; k < 8; ++k)
+            o[k] = pack_half2(__saturatef(__uint_as_float(r[2 * k])), __saturatef(__uint_as_float(r[2 * k + 1])));
+        store_output(p, C.dst, C.valid, C.bad, o);  // R13: clamp [0,1]
         tc_fence_before();
+        C.tile += stride;
+        phase0(C);
+    };
+
+    phase0(cx[0]);
+    phase0(cx[1]);
+    while (cx[0].tile < ntiles || cx[1].tile < ntiles) {
+#pragma unroll
+        for (int layer = 0; layer <= HM; ++layer) {
+            phase_hidden(cx[0], layer);
+            phase_hidden(cx[1], layer);
+        }
+        phase_out(cx[0]);
+        phase_out(cx[1]);
     }
     tc_fence_before();
     __syncthreads();
@@ -387,7 +302,7 @@ __global__ void __launch_bounds__(NWG * 128, 1) decode_kernel(const __grid_const
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-// Tests only: the same addressing + assembly, written to global memory.
+// Tests only: the same addressing + assembly, written to global memory in canonical order.
 template <class P>
 __global__ void debug_assemble_kernel(const __grid_constant__ DecodeParams p) {
     __shared__ __align__(16) uint32_t s_pe[32];
@@ -401,30 +316,46 @@ __global__ void debug_assemble_kernel(const __grid_constant__ DecodeParams p) {
         m = p.M - 1;
         x = y = 0;
     }
+    Fetch<P> f;
+    fetch_texel<P>(p, m, x, y, f, p.dbg_addr + i * 17);
     uint32_t w[P::K1W];
-    assemble_row<P>(p, s_pe, m, x, y, w, p.dbg_addr + i * 17);
+    assemble_words<P>(p, s_pe, f, w);
     uint16_t* X = p.dbg_X + i * P::D;
-    for (int k = 0; k < P::D; ++k) X[k] = (uint16_t)(w[k >> 1] >> (16 * (k & 1)));
+    for (int k = 0; k < P::D; ++k) X[canonical_col<P>(k)] = (uint16_t)(w[k >> 1] >> (16 * (k & 1)));
+}
+
+// Weight image (global copy of the SMEM layout): W1 in K1/64 SW128 atoms of 64 rows with
+// the G0 columns permuted like X and b1 at column D; per hidden layer a weights atom and a
+// bias atom (column 0 = b); W3 (16 rows) and its bias atom.
+template <class P, int HM>
+__global__ void wimg_kernel(const uint16_t* __restrict__ w, int c, uint8_t* __restrict__ img) {
+    using S = DecodeSmem<P, HM>;
+    constexpr int D = P::D, n1 = P::K1_ATOMS * 64 * 64, n2 = 2 * 64 * 64, n3 = 2 * 16 * 64;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n1 + HM * n2 + n3) return;
+    const int P1 = D * HID, P2 = HID * HID;
+    uint16_t v = 0;
+    uint32_t off;
+    if (i < n1) {
+        const int atom = i / 4096, r = (i % 4096) / 64, kk = i % 64, k = atom * 64 + kk;
+        if (k < D) v = w[r * D + canonical_col<P>(k)];
+        else if (k == D) v = w[P1 + r];
+        off = atom * 8192 + sw128_offset(r, kk);
+    } else if (i < n1 + HM * n2) {
+        const int l = (i - n1) / n2, e = (i - n1) % n2, bias = e / 4096, r = (e % 4096) / 64, k = e % 64;
+        const int base = P1 + HID + l * (P2 + HID);
+        v = bias ? (k == 0 ? w[base + P2 + r] : (uint16_t)0) : w[base + r * HID + k];
+        off = S::W1_BYTES + l * S::W2_BYTES + bias * 8192 + sw128_offset(r, k);
+    } else {
+        const int e = i - n1 - HM * n2, bias = e / 1024, r = (e % 1024) / 64, k = e % 64;
+        const int base = P1 + HID + HM * (P2 + HID);
+        if (r < c) v = bias ? (k == 0 ? w[base + HID * c + r] : (uint16_t)0) : w[base + r * HID + k];
+        off = S::W1_BYTES + HM * S::W2_BYTES + bias * 2048 + sw128_offset(r, k);
+    }
+    *reinterpret_cast<uint16_t*>(img + off) = v;
 }
 
 // ------------------------------------------------------------------ launchers
-template <class P, int HM>
-static cudaError_t launch_decode_t(const DecodeParams& p, int grid, cudaStream_t s) {
-    using S = DecodeSmem<P, HM>;
-    auto* k = decode_kernel<P, HM>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
-    if (e != cudaSuccess) return e;
-    k<<<grid, NWG * 128, S::BYTES, s>>>(p);
-    return cudaGetLastError();
-}
-
-template <class P>
-static cudaError_t launch_debug_t(const DecodeParams& p, cudaStream_t s) {
-    const int64_t blocks = (p.nq + 127) / 128;
-    debug_assemble_kernel<P><<<(unsigned)blocks, 128, 0, s>>>(p);
-    return cudaGetLastError();
-}
-
 using NTC02 = Prof<8, 2, 12, 4>;
 using NTC05 = Prof<12, 4, 20, 4>;
 using NTC10 = Prof<12, 2, 10, 4>;
@@ -438,44 +369,54 @@ int profile_id(const ntc_desc* d) {
     return -1;
 }
 
-uint32_t decode_wimg_bytes(int pid, int hm) {
-    switch (pid) {
-        case 0: return hm == 1 ? DecodeSmem<NTC02, 1>::WIMG : DecodeSmem<NTC02, 2>::WIMG;
-        case 1: return hm == 1 ? DecodeSmem<NTC05, 1>::WIMG : DecodeSmem<NTC05, 2>::WIMG;
-        case 2: return hm == 1 ? DecodeSmem<NTC10, 1>::WIMG : DecodeSmem<NTC10, 2>::WIMG;
-        default: return hm == 1 ? DecodeSmem<NTC225, 1>::WIMG : DecodeSmem<NTC225, 2>::WIMG;
+template <class F>
+static auto dispatch(int pid, int hm, F&& f) {
+    switch (pid * 2 + (hm - 1)) {
+        case 0: return f(NTC02{}, std::integral_constant<int, 1>{});
+        case 1: return f(NTC02{}, std::integral_constant<int, 2>{});
+        case 2: return f(NTC05{}, std::integral_constant<int, 1>{});
+        case 3: return f(NTC05{}, std::integral_constant<int, 2>{});
+        case 4: return f(NTC10{}, std::integral_constant<int, 1>{});
+        case 5: return f(NTC10{}, std::integral_constant<int, 2>{});
+        case 6: return f(NTC225{}, std::integral_constant<int, 1>{});
+        default: return f(NTC225{}, std::integral_constant<int, 2>{});
     }
 }
 
-int decode_k1(int pid) {
-    switch (pid) {
-        case 0: return NTC02::K1;
-        case 1: return NTC05::K1;
-        case 2: return NTC10::K1;
-        default: return NTC225::K1;
-    }
+uint32_t decode_wimg_bytes(int pid, int hm) {
+    return dispatch(pid, hm, [](auto pr, auto h) { return DecodeSmem<decltype(pr), decltype(h)::value>::WIMG; });
+}
+
+cudaError_t build_wimg(int pid, int hm, const uint16_t* w, int c, uint8_t* img, cudaStream_t s) {
+    return dispatch(pid, hm, [&](auto pr, auto h) {
+        using PP = decltype(pr);
+        constexpr int HMv = decltype(h)::value;
+        const int n = PP::K1_ATOMS * 4096 + HMv * 8192 + 2048;
+        wimg_kernel<PP, HMv><<<(n + 255) / 256, 256, 0, s>>>(w, c, img);
+        return cudaGetLastError();
+    });
 }
 
 cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cudaStream_t s) {
-    switch (pid * 2 + (hm - 1)) {
-        case 0: return launch_decode_t<NTC02, 1>(p, grid, s);
-        case 1: return launch_decode_t<NTC02, 2>(p, grid, s);
-        case 2: return launch_decode_t<NTC05, 1>(p, grid, s);
-        case 3: return launch_decode_t<NTC05, 2>(p, grid, s);
-        case 4: return launch_decode_t<NTC10, 1>(p, grid, s);
-        case 5: return launch_decode_t<NTC10, 2>(p, grid, s);
-        case 6: return launch_decode_t<NTC225, 1>(p, grid, s);
-        default: return launch_decode_t<NTC225, 2>(p, grid, s);
-    }
+    return dispatch(pid, hm, [&](auto pr, auto h) {
+        using PP = decltype(pr);
+        constexpr int HMv = decltype(h)::value;
+        using SS = DecodeSmem<PP, HMv>;
+        auto* k = decode_kernel<PP, HMv>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
+        if (e != cudaSuccess) return e;
+        k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p);
+        return cudaGetLastError();
+    });
 }
 
 cudaError_t launch_debug_assemble(int pid, const DecodeParams& p, cudaStream_t s) {
-    switch (pid) {
-        case 0: return launch_debug_t<NTC02>(p, s);
-        case 1: return launch_debug_t<NTC05>(p, s);
-        case 2: return launch_debug_t<NTC10>(p, s);
-        default: return launch_debug_t<NTC225>(p, s);
-    }
+    return dispatch(pid, 1, [&](auto pr, auto) {
+        using PP = decltype(pr);
+        const int64_t blocks = (p.nq + 127) / 128;
+        debug_assemble_kernel<PP><<<(unsigned)blocks, 128, 0, s>>>(p);
+        return cudaGetLastError();
+    });
 }
 
 }  // namespace ntc
