@@ -177,9 +177,12 @@ ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const ntc_train_buf
                           const ntc_batch* batch, const ntc_train_hparams* hp, float* loss, int32_t* status,
                           uint32_t flags, ntc_stream stream);
 
-/* Footprint of a batch (host, pure): up to 2*n_crops boxes (level, grid k, x0, y0, x1, y1),
- * inclusive cell ranges of the grids read by the crops' texels.  Returns the box count.   */
-int32_t ntc_train_footprint(const ntc_desc* d, const ntc_batch* batch, int32_t* boxes /* [2*n_crops][6] */);
+/* Footprint of a batch (host, pure): disjoint boxes (level, grid k, x0, y0, x1, y1) of
+ * inclusive cell ranges that together cover exactly the grid cells read by the crops'
+ * texels (at most 64 boxes; a pathological overlap pattern falls back to one bounding box
+ * per grid).  Returns the box count (-1 on a bad batch); pass boxes = NULL to query it,
+ * otherwise boxes must hold [count][6] int32.                                            */
+int32_t ntc_train_footprint(const ntc_desc* d, const ntc_batch* batch, int32_t* boxes);
 
 #ifdef __cplusplus
 }

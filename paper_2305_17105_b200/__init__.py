@@ -276,6 +276,9 @@ def ntc_train_footprint(d, batch):
     import numpy as np
 
     b = batch[0] if isinstance(batch, tuple) else batch
-    boxes = np.zeros((2 * max(1, b.n_crops), 6), np.int32)
-    n = lib().ntc_train_footprint(ctypes.byref(make_desc(d)), ctypes.byref(b), boxes.ctypes.data_as(ctypes.c_void_p))
-    return boxes[:n]
+    n = lib().ntc_train_footprint(ctypes.byref(make_desc(d)), ctypes.byref(b), None)
+    if n < 0:
+        raise NtcError(NTC_ERR_INVALID_ARGUMENT, lib().ntc_last_error().decode())
+    boxes = np.zeros((n, 6), np.int32)
+    lib().ntc_train_footprint(ctypes.byref(make_desc(d)), ctypes.byref(b), boxes.ctypes.data_as(ctypes.c_void_p))
+    return boxes

@@ -41,6 +41,10 @@ static ntc_status cuda_fail(cudaError_t e, const char* what) {
 
 extern "C" const char* ntc_last_error(void) { return g_err.c_str(); }
 
+namespace ntc {
+ntc_status api_fail(ntc_status s, const char* msg) { return fail(s, "%s", msg); }
+}  // namespace ntc
+
 // ------------------------------------------------------------------ geometry
 static int ilog2i(int64_t v) {
     int l = 0;
@@ -283,6 +287,11 @@ extern "C" void ntc_material_destroy(ntc_material* m) {
 
 // ------------------------------------------------------------------ decode
 static double tri_wave(double t) { return 4.0 * std::fabs((t - std::floor(t)) - 0.5) - 1.0; }
+
+namespace ntc {
+uint16_t host_f16(double v) { return float_to_half_bits(v); }
+double host_tri(double t) { return tri_wave(t); }
+}  // namespace ntc
 
 static DecodeParams base_params(const ntc_material* m) {
     DecodeParams p;

@@ -1,0 +1,976 @@
+// train.cu -- NTC compression training step on sm_100a (tcgen05 + TMEM), product code.
+//
+// ntc_train_step(GRADS):
+//   prep_kernel      t2: noisy latents (Philox U(-Q/2,Q/2)) and zeroed latent
+//                    gradients over the batch footprint (disjoint boxes)
+//   train_kernel     t1,t3-t7: per 128-texel tile: fp16 input assembly from the noisy fp32
+//                    latents, forward MLP on tcgen05 (Z kept as fp16 hardGELU' tiles), mean-L2
+//                    loss, backward MMAs (dH2 = d3 W3, dH1 = d2 W2, dX = d1 W1), weight
+//                    gradients accumulated in TMEM across the CTA's tiles as two stacked
+//                    MN-major MMAs, latent-gradient scatter with vector reductions
+//   reduce_kernel    t6: fixed-order sum of the per-warpgroup weight-gradient partials, loss
+// ntc_train_step(APPLY):
+//   adam_kernel      t8: Adam on the weights (dense) and on the footprint latents (sparse:
+//                    g == 0 skipped, R18), then the latent clamp
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace ntc {
+
+constexpr int MAX_BOXES = 64;
+constexpr int TRAIN_WG = 2;  // warpgroups (independent tile pipelines) per CTA
+
+struct Box {        // inclusive cell ranges of one grid
+    int64_t off;    // element offset of the grid in the canonical latent array
+    int32_t r, C, bits;
+    int32_t x0, y0, x1, y1;
+};
+
+struct TrainParams {
+    // geometry of the batch mip
+    int32_t W, c, M, mip, lw;
+    int32_t r0, r1, lr0, lr1;
+    int64_t off0, off1;
+    uint32_t lod_word;
+    uint32_t pe_words[8][4];
+    // batch
+    int32_t n_crops;
+    int32_t crop[NTC_MAX_CROPS][4];
+    int32_t tile_start[NTC_MAX_CROPS + 1];
+    int32_t n_tiles;
+    const uint16_t* ref;
+    int64_t ref_stride;
+    float inv_bc;
+    // buffers
+    const float* noisy;
+    float* grad_lat;
+    const float* params;
+    float* partial;     // [grid * TRAIN_WG][P]
+    float* loss_partial;  // [grid * TRAIN_WG]
+    int32_t P;
+};
+
+// ------------------------------------------------------------------ Philox noise (R16)
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = mulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = mulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+
+struct PrepParams {
+    Box box[MAX_BOXES];
+    int32_t nbox;
+    int32_t box_start[MAX_BOXES + 1];  // prefix of latents per box
+    const float* latents;
+    float* noisy;
+    float* grad_lat;
+    uint64_t seed;
+    uint32_t step;
+    int32_t noise_on;
+};
+
+__device__ __forceinline__ void box_locate(const Box* box, const int32_t* start, int nbox, int32_t i, int& b,
+                                           int64_t& li) {
+    b = 0;
+    while (b + 1 < nbox && i >= start[b + 1]) ++b;
+    const Box& B = box[b];
+    const int32_t k = i - start[b];
+    const int32_t w = (B.x1 - B.x0 + 1) * B.C;
+    const int32_t yy = B.y0 + k / w, rem = k % w;
+    li = B.off + ((int64_t)yy * B.r + B.x0) * B.C + rem;
+}
+
+// t2: noisy = latent + U(-Q/2, Q/2) (one draw per latent per step), grad = 0, over the footprint
+__global__ void prep_kernel(const __grid_constant__ PrepParams p) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.box_start[p.nbox]) return;
+    int b;
+    int64_t li;
+    box_locate(p.box, p.box_start, p.nbox, i, b, li);
+    float v = p.latents[li];
+    if (p.noise_on) {
+        const uint4 r = philox4x32_10(make_uint4((uint32_t)((uint64_t)li >> 2), (uint32_t)((uint64_t)li >> 34), p.step,
+                                                 0x4E4F4953u),
+                                      make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32)));
+        const uint32_t w = (li & 3) == 0 ? r.x : (li & 3) == 1 ? r.y : (li & 3) == 2 ? r.z : r.w;
+        // u = (2 (w >> 9) + 1) 2^-24 in (0, 1); noise = (u - 1/2) Q, exact in fp32
+        const float u = (float)(2u * (w >> 9) + 1u) * 5.9604644775390625e-8f;
+        v += (u - 0.5f) * (1.0f / (float)(1 << p.box[b].bits));
+    }
+    p.noisy[li] = v;
+    p.grad_lat[li] = 0.0f;
+}
+
+// ------------------------------------------------------------------ fused forward + backward
+struct TrainSmem {
+    static constexpr uint32_t W1 = 0, W2 = 8192, W2B = 16384, W3 = 24576, W3B = 26624, WEND = 28672;
+    static constexpr uint32_t TILE = 128 * 128;  // one 128 x 64 fp16 SW128 tile
+    enum { X = 0, H1 = 1, H2 = 2, G1 = 3, G2 = 4, D3 = 5, NT = 6 };
+    static constexpr uint32_t WG_BYTES = NT * TILE;
+    static constexpr uint32_t BYTES = 1024 + WEND + TRAIN_WG * WG_BYTES + 256;
+};
+
+__device__ __forceinline__ void sts_row_chunk(uint32_t tile, int row, int chunk, uint32_t a, uint32_t b, uint32_t c,
+                                              uint32_t d) {
+    sts128(tile + (uint32_t)row * 128u + ((uint32_t)(chunk ^ (row & 7)) << 4), a, b, c, d);
+}
+
+__device__ __forceinline__ uint4 lds_row_chunk(uint32_t tile, int row, int chunk) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(tile + (uint32_t)row * 128u + ((uint32_t)(chunk ^ (row & 7)) << 4)));
+    return v;
+}
+
+__device__ __forceinline__ float hgelu(float z) { return z * __saturatef(fmaf(z, 1.0f / 3.0f, 0.5f)); }
+// R15: derivative of the piecewise hardGELU, the middle piece at +-3/2
+__device__ __forceinline__ float hgelu_d(float z) {
+    const float t = fmaf(z, 2.0f / 3.0f, 0.5f);
+    return z > 1.5f ? 1.0f : (z < -1.5f ? 0.0f : t);
+}
+
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t h2u(float a, float b) { return pack_half2(a, b); }
+
+template <int C0, int C1>
+__global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_constant__ TrainParams p) {
+    using S = TrainSmem;
+    constexpr int D = 4 * C0 + C1 + 13;
+    constexpr int NLAT = 4 * C0 + C1;   // latent columns of X
+    constexpr int KB = D / 16;          // k-step of X holding the constant-1 column D
+    static_assert(D < 64 && NLAT <= 48, "training kernel: K1 = 64 profiles");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::WEND + TRAIN_WG * S::WG_BYTES);
+    float* s_loss = reinterpret_cast<float*>(s_bar + TRAIN_WG);
+    uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_loss + 4);
+    uint32_t* s_tmem = s_pe + 32;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wg = warp >> 2, q = warp & 3, row = q * 32 + lane;
+    const int c = p.c;
+
+    // ---- weight images (fp16, SW128 K-major) from the fp32 master weights; the same images
+    // serve the backward MMAs through MN-major descriptors (W^T without a copy)
+    {
+        const float* w = p.params;
+        const int P1 = D * HID;
+        for (int i = tid; i < 5 * 4096; i += blockDim.x) {
+            const int part = i / 4096, e = i % 4096, r = e / 64, k = e % 64;
+            float v = 0.0f;
+            uint32_t base;
+            if (part == 0) {  // W1 (+ b1 at column D)
+                v = k < D ? w[r * D + k] : (k == D ? w[P1 + r] : 0.0f);
+                base = S::W1;
+            } else if (part == 1) {
+                v = w[P1 + HID + r * HID + k];
+                base = S::W2;
+            } else if (part == 2) {  // b2 at column D (multiplies the 1 of X)
+                v = k == D ? w[P1 + HID + HID * HID + r] : 0.0f;
+                base = S::W2B;
+            } else if (part == 3) {
+                if (r >= 16) continue;
+                v = r < c ? w[P1 + HID + HID * HID + HID + r * HID + k] : 0.0f;
+                base = S::W3;
+            } else {
+                if (r >= 16) continue;
+                v = (r < c && k == D) ? w[P1 + 2 * HID + HID * HID + HID * c + r] : 0.0f;
+                base = S::W3B;
+            }
+            *reinterpret_cast<__half*>(smem + base + sw128_offset(r, k)) = __float2half_rn(v);
+        }
+    }
+    if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
+    if (tid < 4) s_loss[tid] = 0.0f;
+    if (tid == 0) {
+        for (int i = 0; i < TRAIN_WG; ++i) mbar_init(&s_bar[i], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(s_tmem, 512);
+        tmem_relinquish();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    // TMEM per warpgroup: [0,128) dW-a accumulator, [128,144) dW-b, [192,256) scratch
+    const uint32_t tbase = *s_tmem + (uint32_t)wg * 256u;
+    const uint32_t t_acc_a = tbase, t_acc_b = tbase + 128, t_s = tbase + 192;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t tiles = sbase + S::WEND + (uint32_t)wg * S::WG_BYTES;
+    const uint32_t tX = tiles + S::X * S::TILE, tH1 = tiles + S::H1 * S::TILE, tH2 = tiles + S::H2 * S::TILE;
+    const uint32_t tG1 = tiles + S::G1 * S::TILE, tG2 = tiles + S::G2 * S::TILE, tD3 = tiles + S::D3 * S::TILE;
+    const bool issuer = q == 0 && lane == 0;
+    uint64_t* bar = &s_bar[wg];
+    uint32_t phase = 0;
+    auto sync_wg = [&]() {
+        fence_proxy_async_smem();
+        tc_fence_before();
+        named_bar_sync(1 + wg, 128);
+    };
+    auto wait_mma = [&]() {
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+    };
+    const uint64_t dW1 = umma_desc_k_sw128(sbase + S::W1), dW2 = umma_desc_k_sw128(sbase + S::W2);
+    const uint64_t dW2B = umma_desc_k_sw128(sbase + S::W2B), dW3 = umma_desc_k_sw128(sbase + S::W3);
+    const uint64_t dW3B = umma_desc_k_sw128(sbase + S::W3B);
+    const uint64_t dX = umma_desc_k_sw128(tX), dH1 = umma_desc_k_sw128(tH1), dH2 = umma_desc_k_sw128(tH2);
+    const uint64_t dG1 = umma_desc_k_sw128(tG1), dG2 = umma_desc_k_sw128(tG2), dD3 = umma_desc_k_sw128(tD3);
+    // MN-major views: W^T operands and the stacked [X^T; H1^T], [X^T; H2^T], delta^T tiles
+    const uint64_t mW1 = umma_desc_mn_sw128(sbase + S::W1, 8192), mW2 = umma_desc_mn_sw128(sbase + S::W2, 8192);
+    const uint64_t mW3 = umma_desc_mn_sw128(sbase + S::W3, 8192);
+    const uint64_t mXH1 = umma_desc_mn_sw128(tX, tH1 - tX), mXH2 = umma_desc_mn_sw128(tX, tH2 - tX);
+    const uint64_t mG1 = umma_desc_mn_sw128(tG1, S::TILE), mG2 = umma_desc_mn_sw128(tG2, S::TILE);
+    const uint64_t mD3 = umma_desc_mn_sw128(tD3, S::TILE);
+    constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
+    constexpr uint32_t ID64_BT = idesc_f16(128, 64, false, true), ID48_BT = idesc_f16(128, 48, false, true);
+    constexpr uint32_t ID64_AB = idesc_f16(128, 64, true, true), ID16_AB = idesc_f16(128, 16, true, true);
+
+    float loss_acc = 0.0f;
+    bool first = true;
+    const int lw = p.lw;
+
+    for (int tile = blockIdx.x * TRAIN_WG + wg; tile < p.n_tiles; tile += gridDim.x * TRAIN_WG) {
+        // ---- t1: texel of this row
+        int k = 0;
+        while (tile >= p.tile_start[k + 1]) ++k;
+        const int cw = p.crop[k][2], chh = p.crop[k][3];
+        const int li = (tile - p.tile_start[k]) * TILE_M + row;
+        const bool valid = li < cw * chh;
+        const int x = p.crop[k][0] + (valid ? li % cw : 0), y = p.crop[k][1] + (valid ? li / cw : 0);
+        // ---- a1: taps (same integer addressing as decode, R1-R3)
+        int tx0[2], ty0[2], tx1[2], ty1[2];
+        float wt[4];
+        {
+            const int xs = 2 * x + 1, ys = 2 * y + 1;
+            int nx = (xs << p.lr0) - (1 << lw), ny = (ys << p.lr0) - (1 << lw);
+            int i = nx >> (lw + 1), j = ny >> (lw + 1);
+            tx0[0] = max(i, 0);
+            tx0[1] = min(i + 1, p.r0 - 1);
+            ty0[0] = max(j, 0);
+            ty0[1] = min(j + 1, p.r0 - 1);
+            nx = (xs << p.lr1) - (1 << lw);
+            ny = (ys << p.lr1) - (1 << lw);
+            i = nx >> (lw + 1);
+            j = ny >> (lw + 1);
+            const int mask = (2 << lw) - 1;
+            const float ax = (float)(nx & mask) / (float)(2 << lw), ay = (float)(ny & mask) / (float)(2 << lw);
+            wt[0] = (1.0f - ax) * (1.0f - ay);
+            wt[1] = ax * (1.0f - ay);
+            wt[2] = (1.0f - ax) * ay;
+            wt[3] = ax * ay;
+            tx1[0] = max(i, 0);
+            tx1[1] = min(i + 1, p.r1 - 1);
+            ty1[0] = max(j, 0);
+            ty1[1] = min(j + 1, p.r1 - 1);
+        }
+        const float* g0 = p.noisy + p.off0;
+        const float* g1 = p.noisy + p.off1;
+        // ---- t2/a2-a4: X row (canonical column order, R4) -> SW128 tile
+        {
+            uint32_t xw[32];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float* cp = g0 + ((int64_t)ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0;
+#pragma unroll
+                for (int e = 0; e < C0; e += 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(cp + e);
+                    xw[(t * C0 + e) / 2] = h2u(v.x, v.y);
+                    xw[(t * C0 + e) / 2 + 1] = h2u(v.z, v.w);
+                }
+            }
+            {
+                float acc[C1];
+#pragma unroll
+                for (int e = 0; e < C1; ++e) acc[e] = 0.0f;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float* cp = g1 + ((int64_t)ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1;
+#pragma unroll
+                    for (int e = 0; e < C1; e += 4) {
+                        const float4 v = *reinterpret_cast<const float4*>(cp + e);
+                        acc[e] = fmaf(wt[t], v.x, acc[e]);
+                        acc[e + 1] = fmaf(wt[t], v.y, acc[e + 1]);
+                        acc[e + 2] = fmaf(wt[t], v.z, acc[e + 2]);
+                        acc[e + 3] = fmaf(wt[t], v.w, acc[e + 3]);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < C1; e += 2) xw[(4 * C0 + e) / 2] = h2u(acc[e], acc[e + 1]);
+            }
+            constexpr int PEW = NLAT / 2;
+            xw[PEW + 0] = s_pe[4 * (x & 7) + 0];
+            xw[PEW + 1] = s_pe[4 * (x & 7) + 1];
+            xw[PEW + 2] = s_pe[4 * (x & 7) + 2];
+            xw[PEW + 3] = s_pe[4 * (y & 7) + 0];
+            xw[PEW + 4] = s_pe[4 * (y & 7) + 1];
+            xw[PEW + 5] = s_pe[4 * (y & 7) + 2];
+            xw[PEW + 6] = p.lod_word;
+#pragma unroll
+            for (int e = PEW + 7; e < 32; ++e) xw[e] = 0u;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch)
+                sts_row_chunk(tX, row, ch, xw[4 * ch], xw[4 * ch + 1], xw[4 * ch + 2], xw[4 * ch + 3]);
+        }
+        // reference texel (R24: fp16 of v/255 prepared by the caller)
+        float ref[16];
+        {
+            const uint16_t* rp = p.ref + (int64_t)y * p.ref_stride + (int64_t)x * c;
+#pragma unroll
+            for (int o = 0; o < 16; ++o) ref[o] = o < c ? __half2float(__ushort_as_half(rp[o])) : 0.0f;
+        }
+        sync_wg();
+        // ---- t3: forward.  Z1 = X W1^T (+b1)
+        if (issuer) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dX + 2 * kk, dW1 + 2 * kk, ID64, kk > 0);
+            mma_commit(bar);
+        }
+        wait_mma();
+        auto hidden_epilogue = [&](uint32_t tH, uint32_t tG) {
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t r[32];
+                tmem_ld32(t_s + lane_off + 32 * half, r);
+                tmem_wait_ld();
+                uint32_t h[16], g[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
+                    h[i] = h2u(hgelu(z0), hgelu(z1));
+                    g[i] = h2u(hgelu_d(z0), hgelu_d(z1));
+                }
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    sts_row_chunk(tH, row, 4 * half + cc, h[4 * cc], h[4 * cc + 1], h[4 * cc + 2], h[4 * cc + 3]);
+                    sts_row_chunk(tG, row, 4 * half + cc, g[4 * cc], g[4 * cc + 1], g[4 * cc + 2], g[4 * cc + 3]);
+                }
+            }
+        };
+        hidden_epilogue(tH1, tG1);
+        sync_wg();
+        // Z2 = H1 W2^T + b2 (bias through X's constant column)
+        if (issuer) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH1 + 2 * kk, dW2 + 2 * kk, ID64, kk > 0);
+            mma_f16_ss(t_s, dX + 2 * KB, dW2B + 2 * KB, ID64, 1);
+            mma_commit(bar);
+        }
+        wait_mma();
+        hidden_epilogue(tH2, tG2);
+        sync_wg();
+        // Y = H2 W3^T + b3
+        if (issuer) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH2 + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
+            mma_f16_ss(t_s, dX + 2 * KB, dW3B + 2 * KB, ID16, 1);
+            mma_commit(bar);
+        }
+        wait_mma();
+        // ---- t4: mean-L2 loss (R17); delta3 = 2 (y - R) fed unscaled, 1/(B c) applied in fp32
+        {
+            uint32_t r[16];
+            tmem_ld16(t_s + lane_off, r);
+            tmem_wait_ld();
+            float d3[16];
+#pragma unroll
+            for (int o = 0; o < 16; ++o) {
+                const float e = (valid && o < c) ? __uint_as_float(r[o]) - ref[o] : 0.0f;
+                loss_acc = fmaf(e, e, loss_acc);
+                d3[o] = 2.0f * e;
+            }
+            sts_row_chunk(tD3, row, 0, h2u(d3[0], d3[1]), h2u(d3[2], d3[3]), h2u(d3[4], d3[5]), h2u(d3[6], d3[7]));
+            sts_row_chunk(tD3, row, 1, h2u(d3[8], d3[9]), h2u(d3[10], d3[11]), h2u(d3[12], d3[13]),
+                          h2u(d3[14], d3[15]));
+        }
+        sync_wg();
+        // ---- t5: dH2 = d3 W3 ; dW3/db3 += [X^T; H2^T] d3 (stacked, N = 16)
+        if (issuer) {
+            tc_fence_after();
+            mma_f16_ss(t_s, dD3, mW3, ID64_BT, 0);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                mma_f16_ss(t_acc_b, mXH2 + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
+                           (!first || kk > 0) ? 1u : 0u);
+            mma_commit(bar);
+        }
+        wait_mma();
+        auto delta_epilogue = [&](uint32_t tG) {  // delta = dH (TMEM) * hardGELU'(Z) (SMEM), in place
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t r[32];
+                tmem_ld32(t_s + lane_off + 32 * half, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const uint4 gv = lds_row_chunk(tG, row, 4 * half + cc);
+                    const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
+                    uint32_t o[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const __half2 g2 = *reinterpret_cast<const __half2*>(&gw[e]);
+                        const float2 gf = __half22float2(g2);
+                        const int col = 8 * cc + 2 * e;
+                        o[e] = h2u(__uint_as_float(r[col]) * gf.x, __uint_as_float(r[col + 1]) * gf.y);
+                    }
+                    sts_row_chunk(tG, row, 4 * half + cc, o[0], o[1], o[2], o[3]);
+                }
+            }
+        };
+        delta_epilogue(tG2);  // G2 tile now holds delta2
+        sync_wg();
+        // dH1 = d2 W2 ; dW2/db2 += [X^T; H1^T] d2
+        if (issuer) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                mma_f16_ss(t_s, dG2 + 2 * kk, mW2 + (uint64_t)(kk * 128), ID64_BT, kk > 0);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                mma_f16_ss(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
+                           (!first || kk > 0) ? 1u : 0u);
+            mma_commit(bar);
+        }
+        wait_mma();
+        delta_epilogue(tG1);  // G1 tile now holds delta1
+        sync_wg();
+        // dX = d1 W1 (latent columns) ; dW1/db1 += [X^T; H1^T] d1
+        if (issuer) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                mma_f16_ss(t_s, dG1 + 2 * kk, mW1 + (uint64_t)(kk * 128), ID48_BT, kk > 0);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                mma_f16_ss(t_acc_a, mXH1 + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID64_AB,
+                           (!first || kk > 0) ? 1u : 0u);
+            mma_commit(bar);
+        }
+        wait_mma();
+        first = false;
+        // ---- t7: latent-gradient scatter: G0 taps unweighted, G1 taps bilinear-weighted
+        {
+            uint32_t r[48];
+            {
+                uint32_t a[32], b[16];
+                tmem_ld32(t_s + lane_off, a);
+                tmem_ld16(t_s + lane_off + 32, b);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) r[i] = a[i];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) r[32 + i] = b[i];
+            }
+            if (valid) {
+                const float s = p.inv_bc;
+                float* gl0 = p.grad_lat + p.off0;
+                float* gl1 = p.grad_lat + p.off1;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    float* dst = gl0 + ((int64_t)ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0;
+#pragma unroll
+                    for (int e = 0; e < C0; e += 4)
+                        red_add_v4(dst + e, s * __uint_as_float(r[t * C0 + e]), s * __uint_as_float(r[t * C0 + e + 1]),
+                                   s * __uint_as_float(r[t * C0 + e + 2]), s * __uint_as_float(r[t * C0 + e + 3]));
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    float* dst = gl1 + ((int64_t)ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1;
+                    const float sw = s * wt[t];
+                    if (sw != 0.0f) {
+#pragma unroll
+                        for (int e = 0; e < C1; e += 4)
+                            red_add_v4(dst + e, sw * __uint_as_float(r[4 * C0 + e]),
+                                       sw * __uint_as_float(r[4 * C0 + e + 1]), sw * __uint_as_float(r[4 * C0 + e + 2]),
+                                       sw * __uint_as_float(r[4 * C0 + e + 3]));
+                    }
+                }
+            }
+        }
+        tc_fence_before();
+    }
+
+    // ---- t6: this warpgroup's weight-gradient partial (unscaled) + loss partial
+    float* part = p.partial + (size_t)(blockIdx.x * TRAIN_WG + wg) * p.P;
+    {
+        const int P1 = D * HID, o2 = P1 + HID, o3 = o2 + HID * HID + HID;
+        const int m = row;  // stacked rows: [0,64) X features, [64,128) H units
+        if (first) {  // no tile processed: zero partial
+            for (int i = row; i < p.P; i += 128) part[i] = 0.0f;
+        } else {
+#pragma unroll
+            for (int blk = 0; blk < 4; ++blk) {
+                uint32_t r[32];
+                tmem_ld32(t_acc_a + lane_off + 32 * blk, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int col = 32 * blk + e;
+                    const float v = __uint_as_float(r[e]);
+                    if (m < 64) {
+                        if (col < 64) {
+                            if (m < D) part[col * D + m] = v;          // dW1[j][i]
+                            else if (m == D) part[P1 + col] = v;       // db1[j]
+                        } else if (m == D) {
+                            part[o2 + HID * HID + (col - 64)] = v;     // db2[j]
+                        }
+                    } else if (col >= 64) {
+                        part[o2 + (col - 64) * HID + (m - 64)] = v;    // dW2[j][i]
+                    }
+                }
+            }
+            uint32_t r[16];
+            tmem_ld16(t_acc_b + lane_off, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int o = 0; o < 16; ++o) {
+                if (o >= c) continue;
+                const float v = __uint_as_float(r[o]);
+                if (m == D) part[o3 + HID * c + o] = v;                // db3[o]
+                else if (m >= 64) part[o3 + o * HID + (m - 64)] = v;   // dW3[o][i]
+            }
+        }
+    }
+    {
+        float v = loss_acc;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+        if (lane == 0) atomicAdd(&s_loss[wg], v);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid < TRAIN_WG) p.loss_partial[blockIdx.x * TRAIN_WG + tid] = s_loss[tid];
+    if (warp == 0) tmem_dealloc(*s_tmem, 512);
+}
+
+// fixed-order reduction of the partials (deterministic), scaled by 1/(B c)
+__global__ void reduce_kernel(const float* __restrict__ partial, const float* __restrict__ loss_partial, int nparts,
+                              int P, float inv_bc, float* __restrict__ grad, float* __restrict__ loss,
+                              int32_t* __restrict__ status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P) {
+        float s = 0.0f;
+        for (int w = 0; w < nparts; ++w) s += partial[(size_t)w * P + i];
+        grad[i] = s * inv_bc;
+    }
+    if (i == 0) {
+        float s = 0.0f;
+        for (int w = 0; w < nparts; ++w) s += loss_partial[w];
+        const float l = s * inv_bc;
+        *loss = l;
+        if (!isfinite(l) && status) atomicOr(status, (int)NTC_ERR_NONFINITE);
+    }
+}
+
+// ------------------------------------------------------------------ t8: Adam + clamp
+struct AdamParams {
+    Box box[MAX_BOXES];
+    int32_t nbox;
+    int32_t box_start[MAX_BOXES + 1];
+    int32_t dense_latents;
+    int64_t n_latents;
+    int32_t P;
+    float* params;
+    float* m_par;
+    float* v_par;
+    const float* grad_par;
+    float* latents;
+    float* m_lat;
+    float* v_lat;
+    const float* grad_lat;
+    float lr_w, lr_l, b1, b2, eps, c1, c2;  // c1 = 1 - b1^t, c2 = 1 - b2^t
+    // dense-latent mode: per-grid bits lookup
+    int32_t ngrid;
+    int64_t grid_start[2 * MAX_LEVELS + 1];
+    int32_t grid_bits[2 * MAX_LEVELS];
+};
+
+__device__ __forceinline__ void adam_one(float& p, float& m, float& v, float g, float lr, const AdamParams& a) {
+    m = a.b1 * m + (1.0f - a.b1) * g;
+    v = a.b2 * v + (1.0f - a.b2) * g * g;
+    p -= lr * (m / a.c1) / (sqrtf(v / a.c2) + a.eps);
+}
+
+__global__ void adam_kernel(const __grid_constant__ AdamParams a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < a.P) {  // weights: dense
+        float p = a.params[i], m = a.m_par[i], v = a.v_par[i];
+        adam_one(p, m, v, a.grad_par[i], a.lr_w, a);
+        a.params[i] = p;
+        a.m_par[i] = m;
+        a.v_par[i] = v;
+        return;
+    }
+    const int64_t j = i - a.P;
+    int64_t li;
+    int bits;
+    if (a.dense_latents) {
+        if (j >= a.n_latents) return;
+        li = j;
+        int g = 0;
+        while (li >= a.grid_start[g + 1]) ++g;
+        bits = a.grid_bits[g];
+    } else {
+        if (j >= a.box_start[a.nbox]) return;
+        int b;
+        box_locate(a.box, a.box_start, a.nbox, (int32_t)j, b, li);
+        bits = a.box[b].bits;
+    }
+    const float g = a.grad_lat[li];
+    if (!a.dense_latents && g == 0.0f) return;  // R18: footprint-sparse Adam skips g == 0
+    float p = a.latents[li], m = a.m_lat[li], v = a.v_lat[li];
+    adam_one(p, m, v, g, a.lr_l, a);
+    const float N = (float)(1 << bits);
+    p = fminf(fmaxf(p, -(N - 1.0f) / (2.0f * N)), 0.5f);  // clamp to [-(N-1)Q/2, NQ/2]
+    a.latents[li] = p;
+    a.m_lat[li] = m;
+    a.v_lat[li] = v;
+}
+
+}  // namespace ntc
+
+// ====================================================================== host side
+using namespace ntc;
+
+extern "C" int32_t ntc_num_mips(const ntc_desc* d);
+extern "C" int32_t ntc_num_levels(const ntc_desc* d);
+extern "C" int32_t ntc_level_of_mip(const ntc_desc* d, int32_t mip);
+extern "C" int64_t ntc_num_latents(const ntc_desc* d);
+extern "C" int64_t ntc_num_params(const ntc_desc* d);
+extern "C" ntc_status ntc_grid_layout(const ntc_desc* d, int32_t level, int32_t* r0, int32_t* r1, int64_t* off0,
+                                      int64_t* off1);
+namespace ntc {
+ntc_status api_fail(ntc_status s, const char* msg);
+uint16_t host_f16(double v);
+double host_tri(double t);
+}  // namespace ntc
+
+struct ntc_trainer {
+    ntc_desc d;
+    int num_sms = 148;
+    float* partial = nullptr;
+    float* loss_partial = nullptr;
+};
+
+static int ilog2_t(int64_t v) {
+    int l = 0;
+    while ((int64_t(1) << (l + 1)) <= v) ++l;
+    return l;
+}
+
+extern "C" ntc_status ntc_trainer_create(const ntc_desc* d, ntc_trainer** out) {
+    if (!d || !out) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!(d->c0 == 8 && d->b0 == 2 && d->c1 == 12 && d->b1 == 4) || d->hidden_mats != 1 || d->activation != 0)
+        return api_fail(NTC_ERR_UNSUPPORTED, "training kernel compiled for NTC 0.2, [D,64,64,c], hardGELU");
+    if (d->channels < 1 || d->channels > 16 || d->width < 8 || (d->width & (d->width - 1)) ||
+        d->width > (1 << 15))
+        return api_fail(NTC_ERR_INVALID_ARGUMENT, "bad texture dims");
+    auto* t = new ntc_trainer();
+    t->d = *d;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t P = ntc_num_params(d);
+    cudaError_t e = cudaMalloc(&t->partial, sizeof(float) * P * t->num_sms * TRAIN_WG);
+    if (e == cudaSuccess) e = cudaMalloc(&t->loss_partial, sizeof(float) * t->num_sms * TRAIN_WG);
+    if (e != cudaSuccess) {
+        ntc_trainer_destroy(t);
+        return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
+    }
+    *out = t;
+    return NTC_OK;
+}
+
+extern "C" void ntc_trainer_destroy(ntc_trainer* t) {
+    if (!t) return;
+    if (t->partial) cudaFree(t->partial);
+    if (t->loss_partial) cudaFree(t->loss_partial);
+    delete t;
+}
+
+// inclusive tap range [lo, hi] of a grid of resolution r over texels [a, b] of a mip of width 2^lw
+static void tap_range(int a, int b, int r, int lw, int* lo, int* hi) {
+    const int lr = ilog2_t(r);
+    const int na = ((2 * a + 1) << lr) - (1 << lw), nb = ((2 * b + 1) << lr) - (1 << lw);
+    *lo = std::max(na >> (lw + 1), 0);
+    *hi = std::min((nb >> (lw + 1)) + 1, r - 1);
+}
+
+struct Rect {
+    int x0, y0, x1, y1;
+};
+
+// r minus s as up to four disjoint rectangles
+static void rect_subtract(const Rect& r, const Rect& s, std::vector<Rect>& out) {
+    if (s.x1 < r.x0 || s.x0 > r.x1 || s.y1 < r.y0 || s.y0 > r.y1) {
+        out.push_back(r);
+        return;
+    }
+    if (s.y0 > r.y0) out.push_back({r.x0, r.y0, r.x1, s.y0 - 1});
+    if (s.y1 < r.y1) out.push_back({r.x0, s.y1 + 1, r.x1, r.y1});
+    const int ya = std::max(r.y0, s.y0), yb = std::min(r.y1, s.y1);
+    if (s.x0 > r.x0) out.push_back({r.x0, ya, s.x0 - 1, yb});
+    if (s.x1 < r.x1) out.push_back({s.x1 + 1, ya, r.x1, yb});
+}
+
+static ntc_status check_batch(const ntc_desc* d, const ntc_batch* b) {
+    if (!b || b->n_crops < 1 || b->n_crops > NTC_MAX_CROPS || !b->crops)
+        return api_fail(NTC_ERR_INVALID_ARGUMENT, "bad batch (1 <= n_crops <= NTC_MAX_CROPS)");
+    if (b->mip < 0 || b->mip >= ntc_num_mips(d)) return api_fail(NTC_ERR_INVALID_ARGUMENT, "batch mip out of range");
+    const int wm = d->width >> b->mip;
+    for (int k = 0; k < b->n_crops; ++k) {
+        const int* c = b->crops + 4 * k;
+        if (c[2] < 1 || c[3] < 1 || c[0] < 0 || c[1] < 0 || c[0] + c[2] > wm || c[1] + c[3] > wm)
+            return api_fail(NTC_ERR_INVALID_ARGUMENT, "crop outside the mip");
+    }
+    return NTC_OK;
+}
+
+// disjoint footprint boxes of a batch (both grids of the batch's level)
+static std::vector<Box> footprint(const ntc_desc* d, const ntc_batch* b) {
+    const int j = ntc_level_of_mip(d, b->mip);
+    int32_t r[2];
+    int64_t off[2];
+    ntc_grid_layout(d, j, &r[0], &r[1], &off[0], &off[1]);
+    const int lw = ilog2_t(d->width >> b->mip);
+    std::vector<Box> boxes;
+    for (int k = 0; k < 2; ++k) {
+        std::vector<Rect> acc;
+        for (int ci = 0; ci < b->n_crops; ++ci) {
+            const int* c = b->crops + 4 * ci;
+            Rect nr;
+            tap_range(c[0], c[0] + c[2] - 1, r[k], lw, &nr.x0, &nr.x1);
+            tap_range(c[1], c[1] + c[3] - 1, r[k], lw, &nr.y0, &nr.y1);
+            std::vector<Rect> pieces{nr};
+            for (const Rect& s : acc) {
+                std::vector<Rect> nxt;
+                for (const Rect& pc : pieces) rect_subtract(pc, s, nxt);
+                pieces.swap(nxt);
+            }
+            acc.insert(acc.end(), pieces.begin(), pieces.end());
+        }
+        for (const Rect& q : acc)
+            boxes.push_back(Box{off[k], r[k], k ? d->c1 : d->c0, k ? d->b1 : d->b0, q.x0, q.y0, q.x1, q.y1});
+    }
+    if ((int)boxes.size() > MAX_BOXES) {  // degenerate overlap pattern: one bounding box per grid
+        std::vector<Box> bb;
+        for (int k = 0; k < 2; ++k) {
+            Box u{off[k], r[k], k ? d->c1 : d->c0, k ? d->b1 : d->b0, 1 << 30, 1 << 30, -1, -1};
+            for (const Box& x : boxes)
+                if (x.off == off[k]) {
+                    u.x0 = std::min(u.x0, x.x0);
+                    u.y0 = std::min(u.y0, x.y0);
+                    u.x1 = std::max(u.x1, x.x1);
+                    u.y1 = std::max(u.y1, x.y1);
+                }
+            bb.push_back(u);
+        }
+        boxes.swap(bb);
+    }
+    return boxes;
+}
+
+extern "C" int32_t ntc_train_footprint(const ntc_desc* d, const ntc_batch* batch, int32_t* out) {
+    if (!d || check_batch(d, batch) != NTC_OK) return -1;
+    const std::vector<Box> boxes = footprint(d, batch);
+    if (out) {
+        const int L = ntc_num_levels(d);
+        for (size_t i = 0; i < boxes.size(); ++i) {
+            int level = 0, k = 0;
+            for (int j = 0; j < L; ++j) {
+                int32_t r0, r1;
+                int64_t o0, o1;
+                ntc_grid_layout(d, j, &r0, &r1, &o0, &o1);
+                if (boxes[i].off == o0) level = j, k = 0;
+                if (boxes[i].off == o1) level = j, k = 1;
+            }
+            int32_t* o = out + 6 * i;
+            o[0] = level;
+            o[1] = k;
+            o[2] = boxes[i].x0;
+            o[3] = boxes[i].y0;
+            o[4] = boxes[i].x1;
+            o[5] = boxes[i].y1;
+        }
+    }
+    return (int32_t)boxes.size();
+}
+
+static int32_t box_prefix(const std::vector<Box>& boxes, Box* dst, int32_t* start) {
+    int64_t acc = 0;
+    for (size_t i = 0; i < boxes.size(); ++i) {
+        dst[i] = boxes[i];
+        start[i] = (int32_t)acc;
+        acc += (int64_t)(boxes[i].x1 - boxes[i].x0 + 1) * (boxes[i].y1 - boxes[i].y0 + 1) * boxes[i].C;
+    }
+    start[boxes.size()] = (int32_t)acc;
+    return (int32_t)acc;
+}
+
+extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const ntc_train_buffers* buf,
+                                     const ntc_batch* batch, const ntc_train_hparams* hp, float* loss,
+                                     int32_t* status, uint32_t flags, ntc_stream stream) {
+    if (!t || !d || !buf || !hp) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (memcmp(&t->d, d, sizeof(ntc_desc)) != 0) return api_fail(NTC_ERR_INVALID_ARGUMENT, "desc != trainer desc");
+    if (ntc_status s = check_batch(d, batch)) return s;
+    if (hp->step < 1) return api_fail(NTC_ERR_INVALID_ARGUMENT, "step must be >= 1");
+    cudaStream_t st = (cudaStream_t)stream;
+    const std::vector<Box> boxes = footprint(d, batch);
+    const int64_t P = ntc_num_params(d), NL = ntc_num_latents(d);
+    cudaError_t e = cudaSuccess;
+    if (flags & NTC_STEP_GRADS) {
+        if (!buf->latents || !buf->noisy || !buf->grad_lat || !buf->params || !buf->grad_par || !loss || !batch->ref)
+            return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+        // t2: noisy latents + zeroed gradients over the footprint
+        PrepParams pp;
+        memset(&pp, 0, sizeof pp);
+        pp.nbox = (int32_t)boxes.size();
+        const int32_t n = box_prefix(boxes, pp.box, pp.box_start);
+        pp.latents = buf->latents;
+        pp.noisy = buf->noisy;
+        pp.grad_lat = buf->grad_lat;
+        pp.seed = hp->seed;
+        pp.step = (uint32_t)hp->step;
+        pp.noise_on = hp->noise_on;
+        if (hp->dense_latent_adam) cudaMemsetAsync(buf->grad_lat, 0, sizeof(float) * NL, st);
+        prep_kernel<<<(n + 255) / 256, 256, 0, st>>>(pp);
+        // t1, t3-t7
+        TrainParams tp;
+        memset(&tp, 0, sizeof tp);
+        const int m = batch->mip;
+        const int j = ntc_level_of_mip(d, m);
+        int32_t r0, r1;
+        int64_t o0, o1;
+        ntc_grid_layout(d, j, &r0, &r1, &o0, &o1);
+        tp.W = d->width;
+        tp.c = d->channels;
+        tp.M = ntc_num_mips(d);
+        tp.mip = m;
+        tp.lw = tp.M - 1 - m;
+        tp.r0 = r0;
+        tp.r1 = r1;
+        tp.lr0 = ilog2_t(r0);
+        tp.lr1 = ilog2_t(r1);
+        tp.off0 = o0;
+        tp.off1 = o1;
+        const double lod = tp.M > 1 ? (double)m / (double)(tp.M - 1) : 0.0;  // R6
+        tp.lod_word = (uint32_t)host_f16(lod) | ((uint32_t)host_f16(1.0) << 16);
+        for (int qq = 0; qq < 8; ++qq) {
+            uint16_t v[6];
+            for (int h = 0; h < 3; ++h) {
+                const double tt = (double)(1 << h) * qq / 8.0;
+                v[2 * h] = host_f16(host_tri(tt));
+                v[2 * h + 1] = host_f16(host_tri(tt - 0.25));
+            }
+            for (int k = 0; k < 3; ++k) tp.pe_words[qq][k] = (uint32_t)v[2 * k] | ((uint32_t)v[2 * k + 1] << 16);
+        }
+        tp.n_crops = batch->n_crops;
+        int64_t B = 0, tiles = 0;
+        for (int k = 0; k < batch->n_crops; ++k) {
+            for (int f = 0; f < 4; ++f) tp.crop[k][f] = batch->crops[4 * k + f];
+            tp.tile_start[k] = (int32_t)tiles;
+            const int64_t area = (int64_t)batch->crops[4 * k + 2] * batch->crops[4 * k + 3];
+            B += area;
+            tiles += (area + TILE_M - 1) / TILE_M;
+        }
+        for (int k = batch->n_crops; k <= NTC_MAX_CROPS; ++k) tp.tile_start[k] = INT32_MAX;
+        tp.tile_start[batch->n_crops] = (int32_t)tiles;
+        tp.n_tiles = (int32_t)tiles;
+        tp.ref = batch->ref;
+        tp.ref_stride = batch->ref_row_stride_elems;
+        tp.inv_bc = (float)(1.0 / ((double)B * d->channels));
+        tp.noisy = buf->noisy;
+        tp.grad_lat = buf->grad_lat;
+        tp.params = buf->params;
+        tp.partial = t->partial;
+        tp.loss_partial = t->loss_partial;
+        tp.P = (int32_t)P;
+        const int grid = (int)std::min<int64_t>(t->num_sms, (tiles + TRAIN_WG - 1) / TRAIN_WG);
+        auto* k = train_kernel<8, 12>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TrainSmem::BYTES);
+        if (e == cudaSuccess) {
+            k<<<grid, TRAIN_WG * 128, TrainSmem::BYTES, st>>>(tp);
+            // t6: deterministic cross-CTA reduction, scaled by 1/(B c)
+            reduce_kernel<<<(int)((P + 255) / 256), 256, 0, st>>>(t->partial, t->loss_partial, grid * TRAIN_WG,
+                                                                   (int)P, tp.inv_bc, buf->grad_par, loss, status);
+            e = cudaGetLastError();
+        }
+        if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (flags & NTC_STEP_APPLY) {
+        if (!buf->latents || !buf->m_lat || !buf->v_lat || !buf->grad_lat || !buf->params || !buf->m_par ||
+            !buf->v_par || !buf->grad_par)
+            return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+        AdamParams a;
+        memset(&a, 0, sizeof a);
+        a.nbox = (int32_t)boxes.size();
+        const int32_t n = box_prefix(boxes, a.box, a.box_start);
+        a.dense_latents = hp->dense_latent_adam;
+        a.n_latents = NL;
+        a.P = (int32_t)P;
+        a.params = buf->params;
+        a.m_par = buf->m_par;
+        a.v_par = buf->v_par;
+        a.grad_par = buf->grad_par;
+        a.latents = buf->latents;
+        a.m_lat = buf->m_lat;
+        a.v_lat = buf->v_lat;
+        a.grad_lat = buf->grad_lat;
+        a.lr_w = hp->lr_weight;
+        a.lr_l = hp->lr_latent;
+        a.b1 = hp->beta1;
+        a.b2 = hp->beta2;
+        a.eps = hp->eps;
+        a.c1 = (float)(1.0 - std::pow((double)hp->beta1, (double)hp->step));
+        a.c2 = (float)(1.0 - std::pow((double)hp->beta2, (double)hp->step));
+        const int L = ntc_num_levels(d);
+        a.ngrid = 2 * L;
+        int64_t acc = 0;
+        for (int j = 0; j < L; ++j) {
+            int32_t r0, r1;
+            int64_t o0, o1;
+            ntc_grid_layout(d, j, &r0, &r1, &o0, &o1);
+            a.grid_start[2 * j] = o0;
+            a.grid_bits[2 * j] = d->b0;
+            a.grid_start[2 * j + 1] = o1;
+            a.grid_bits[2 * j + 1] = d->b1;
+            acc = o1 + (int64_t)r1 * r1 * d->c1;
+        }
+        a.grid_start[2 * L] = acc;
+        const int64_t total = P + (hp->dense_latent_adam ? NL : (int64_t)n);
+        adam_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
+    }
+    return NTC_OK;
+}

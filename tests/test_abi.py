@@ -88,3 +88,33 @@ def test_product_has_no_oracle_dependency():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "ntc_oracle" not in txt and "ntco_" not in txt, f
+
+
+@pytest.mark.parametrize("mip", [0, 1, 3, 5])
+def test_train_footprint_matches_oracle(O, libpath, mip):
+    """Host footprint boxes (disjoint) cover exactly the latent cells the batch reads
+    according to the oracle's addressing."""
+    import numpy as np
+
+    from paper_2305_17105_b200.synth import gen_crops
+
+    d = Profile.named("ntc0.2", 128, 8)
+    crops = gen_crops(3 + mip, 128, mip, 5, 24 >> min(mip, 2))
+    b = ntc.make_batch(mip, crops, None, 0)
+    boxes = ntc.ntc_train_footprint(d, b)
+    got = set()
+    for lvl, k, x0, y0, x1, y1 in boxes:
+        for y in range(y0, y1 + 1):
+            for x in range(x0, x1 + 1):
+                cell = (lvl, k, x, y)
+                assert cell not in got  # disjoint
+                got.add(cell)
+    want = set()
+    for x0, y0, w, h in crops:
+        for y in range(y0, y0 + h):
+            for x in range(x0, x0 + w):
+                ti, _ = O.address(d, mip, x, y)
+                for t in range(4):
+                    want.add((ti[0], 0, ti[1 + 2 * t], ti[2 + 2 * t]))
+                    want.add((ti[0], 1, ti[9 + 2 * t], ti[10 + 2 * t]))
+    assert got == want
