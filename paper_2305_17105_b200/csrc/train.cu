@@ -52,7 +52,7 @@ struct TrainParams {
     // buffers
     const float* noisy;
     float* grad_lat;
-    const float* params;
+    const uint8_t* wimg;  // fp16 weight image (TrainSmem layout, WEND bytes)
     float* partial;     // [grid * TRAIN_WG][P]
     float* loss_partial;  // [grid * TRAIN_WG]
     int32_t P;
@@ -153,6 +153,37 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 
 __device__ __forceinline__ uint32_t h2u(float a, float b) { return pack_half2(a, b); }
 
+// fp16 SW128 weight image of the current fp32 master weights (t3): W1 (+ b1 at column D),
+// W2, b2 at column D of a bias atom (it multiplies X's constant 1), W3 (16 rows), b3 atom
+__global__ void train_wimg_kernel(const float* __restrict__ w, int D, int c, uint8_t* __restrict__ img) {
+    using S = TrainSmem;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 5 * 4096) return;
+    const int P1 = D * HID;
+    const int part = i / 4096, e = i % 4096, r = e / 64, k = e % 64;
+    float v = 0.0f;
+    uint32_t base;
+    if (part == 0) {
+        v = k < D ? w[r * D + k] : (k == D ? w[P1 + r] : 0.0f);
+        base = S::W1;
+    } else if (part == 1) {
+        v = w[P1 + HID + r * HID + k];
+        base = S::W2;
+    } else if (part == 2) {
+        v = k == D ? w[P1 + HID + HID * HID + r] : 0.0f;
+        base = S::W2B;
+    } else if (part == 3) {
+        if (r >= 16) return;
+        v = r < c ? w[P1 + HID + HID * HID + HID + r * HID + k] : 0.0f;
+        base = S::W3;
+    } else {
+        if (r >= 16) return;
+        v = (r < c && k == D) ? w[P1 + 2 * HID + HID * HID + HID * c + r] : 0.0f;
+        base = S::W3B;
+    }
+    *reinterpret_cast<__half*>(img + base + sw128_offset(r, k)) = __float2half_rn(v);
+}
+
 template <int C0, int C1>
 __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_constant__ TrainParams p) {
     using S = TrainSmem;
@@ -171,36 +202,10 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     const int wg = warp >> 2, q = warp & 3, row = q * 32 + lane;
     const int c = p.c;
 
-    // ---- weight images (fp16, SW128 K-major) from the fp32 master weights; the same images
-    // serve the backward MMAs through MN-major descriptors (W^T without a copy)
-    {
-        const float* w = p.params;
-        const int P1 = D * HID;
-        for (int i = tid; i < 5 * 4096; i += blockDim.x) {
-            const int part = i / 4096, e = i % 4096, r = e / 64, k = e % 64;
-            float v = 0.0f;
-            uint32_t base;
-            if (part == 0) {  // W1 (+ b1 at column D)
-                v = k < D ? w[r * D + k] : (k == D ? w[P1 + r] : 0.0f);
-                base = S::W1;
-            } else if (part == 1) {
-                v = w[P1 + HID + r * HID + k];
-                base = S::W2;
-            } else if (part == 2) {  // b2 at column D (multiplies the 1 of X)
-                v = k == D ? w[P1 + HID + HID * HID + r] : 0.0f;
-                base = S::W2B;
-            } else if (part == 3) {
-                if (r >= 16) continue;
-                v = r < c ? w[P1 + HID + HID * HID + HID + r * HID + k] : 0.0f;
-                base = S::W3;
-            } else {
-                if (r >= 16) continue;
-                v = (r < c && k == D) ? w[P1 + 2 * HID + HID * HID + HID * c + r] : 0.0f;
-                base = S::W3B;
-            }
-            *reinterpret_cast<__half*>(smem + base + sw128_offset(r, k)) = __float2half_rn(v);
-        }
-    }
+    // ---- weight images (fp16, SW128 K-major, built once per step by train_wimg_kernel); the
+    // same images serve the backward MMAs through MN-major descriptors (W^T without a copy)
+    for (uint32_t i = tid; i < S::WEND / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.wimg) + i);
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
     if (tid < 4) s_loss[tid] = 0.0f;
     if (tid == 0) {
@@ -573,20 +578,30 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     if (warp == 0) tmem_dealloc(*s_tmem, 512);
 }
 
-// fixed-order reduction of the partials (deterministic), scaled by 1/(B c)
+// fixed-order reduction of the partials (deterministic), scaled by 1/(B c): block = 32
+// parameters x 8 partial groups; group g sums partials g, g+8, ...; the 8 group sums are
+// then added in order.
 __global__ void reduce_kernel(const float* __restrict__ partial, const float* __restrict__ loss_partial, int nparts,
                               int P, float inv_bc, float* __restrict__ grad, float* __restrict__ loss,
                               int32_t* __restrict__ status) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < P) {
-        float s = 0.0f;
-        for (int w = 0; w < nparts; ++w) s += partial[(size_t)w * P + i];
-        grad[i] = s * inv_bc;
+    __shared__ float s[8][33];
+    const int px = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int i = blockIdx.x * 32 + px;
+    float acc = 0.0f;
+    if (i < P)
+        for (int w = g; w < nparts; w += 8) acc += __ldg(partial + (size_t)w * P + i);
+    s[g][px] = acc;
+    __syncthreads();
+    if (g == 0 && i < P) {
+        float t = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += s[k][px];
+        grad[i] = t * inv_bc;
     }
-    if (i == 0) {
-        float s = 0.0f;
-        for (int w = 0; w < nparts; ++w) s += loss_partial[w];
-        const float l = s * inv_bc;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        float t = 0.0f;
+        for (int w = 0; w < nparts; ++w) t += loss_partial[w];
+        const float l = t * inv_bc;
         *loss = l;
         if (!isfinite(l) && status) atomicOr(status, (int)NTC_ERR_NONFINITE);
     }
@@ -680,6 +695,7 @@ struct ntc_trainer {
     int num_sms = 148;
     float* partial = nullptr;
     float* loss_partial = nullptr;
+    uint8_t* wimg = nullptr;
 };
 
 static int ilog2_t(int64_t v) {
@@ -703,6 +719,8 @@ extern "C" ntc_status ntc_trainer_create(const ntc_desc* d, ntc_trainer** out) {
     const int64_t P = ntc_num_params(d);
     cudaError_t e = cudaMalloc(&t->partial, sizeof(float) * P * t->num_sms * TRAIN_WG);
     if (e == cudaSuccess) e = cudaMalloc(&t->loss_partial, sizeof(float) * t->num_sms * TRAIN_WG);
+    if (e == cudaSuccess) e = cudaMalloc(&t->wimg, TrainSmem::WEND);
+    if (e == cudaSuccess) e = cudaMemset(t->wimg, 0, TrainSmem::WEND);
     if (e != cudaSuccess) {
         ntc_trainer_destroy(t);
         return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
@@ -715,6 +733,7 @@ extern "C" void ntc_trainer_destroy(ntc_trainer* t) {
     if (!t) return;
     if (t->partial) cudaFree(t->partial);
     if (t->loss_partial) cudaFree(t->loss_partial);
+    if (t->wimg) cudaFree(t->wimg);
     delete t;
 }
 
@@ -911,7 +930,9 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.inv_bc = (float)(1.0 / ((double)B * d->channels));
         tp.noisy = buf->noisy;
         tp.grad_lat = buf->grad_lat;
-        tp.params = buf->params;
+        tp.wimg = t->wimg;
+        train_wimg_kernel<<<(5 * 4096 + 255) / 256, 256, 0, st>>>(buf->params, 4 * d->c0 + d->c1 + 13, d->channels,
+                                                                 t->wimg);
         tp.partial = t->partial;
         tp.loss_partial = t->loss_partial;
         tp.P = (int32_t)P;
@@ -921,7 +942,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         if (e == cudaSuccess) {
             k<<<grid, TRAIN_WG * 128, TrainSmem::BYTES, st>>>(tp);
             // t6: deterministic cross-CTA reduction, scaled by 1/(B c)
-            reduce_kernel<<<(int)((P + 255) / 256), 256, 0, st>>>(t->partial, t->loss_partial, grid * TRAIN_WG,
+            reduce_kernel<<<(int)((P + 31) / 32), 256, 0, st>>>(t->partial, t->loss_partial, grid * TRAIN_WG,
                                                                    (int)P, tp.inv_bc, buf->grad_par, loss, status);
             e = cudaGetLastError();
         }
