@@ -126,7 +126,7 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_2305_17105_b200 as ntc
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
     d = Profile.named("ntc0.2", W, C)
@@ -156,11 +156,20 @@ def run_ours(args, rank, world, local_rank):
         if e.status != ntc.NTC_ERR_UNSUPPORTED:
             raise
 
-    crop_sets = [gen_crops(seed + 100 + i, W, 0, 4, 256) for i in range(args.warmup + args.steps)]
+    # weak scaling: 4 crops of 256^2 per rank; all ranks draw the same global crop list
+    crop_sets = [gen_crops(SEED_BASE + 3 + 1000 * i, W, 0, 4 * world, 256) for i in range(args.warmup + args.steps)]
+    dp = None
+    if train is not None and world > 1:
+        from paper_2305_17105_b200.dist import DataParallelTrainer
+
+        dp = DataParallelTrainer(d, train["tb"]["latents"], train["tb"]["params"])
 
     def train_step(i):
-        batch = ntc.make_batch(0, crop_sets[i], train["ref"], W * C)
         hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, i + 1, seed, 1, 0)
+        if dp is not None:  # data-parallel: GRADS on own crops, one all-reduce, APPLY
+            dp.step(0, crop_sets[i], train["ref"], W * C, hp)
+            return
+        batch = ntc.make_batch(0, crop_sets[i], train["ref"], W * C)
         ntc.ntc_train_step(train["tr"], train["buf"], batch, hp, train["loss"], train["status"])
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -218,13 +227,15 @@ def run_ours(args, rank, world, local_rank):
                      "frac": round(achieved / peak_tf, 4), "traffic": tr_bytes,
                      "peak_source": f"{pk_src} bf16 dense burst (fp16 same rate)",
                      "kernel": "ntc::decode_kernel", "flops_per_texel": decode_flops_per_texel(d)},
-        "gpu_launches": args.steps * (1 + (5 if train is not None else 0)),
+        "gpu_launches": args.steps * (1 + (0 if train is None else (5 if world == 1 else 8))),
         "clocks": clk.report(),
     })
     if train is not None:
         B = 4 * 256 * 256
         tflops = train_flops_per_texel(d) * B / (trn / args.steps) / 1e12
         res["train"] = {"metric": "training texels/s", "value": B * world * args.steps / trn,
+                        "parallelism": "single GPU" if world == 1 else
+                        f"data-parallel x{world}: 4 crops/rank, one NCCL all-reduce of [dW | loss | footprint dLatent]",
                         "unit": "texel/s", "ms_per_step": trn / args.steps * 1e3, "workload": TRAIN_WORKLOAD,
                         "roofline": {"bound": "tensor", "achieved": round(tflops, 2), "peak": peak_tf,
                                      "unit": "TFLOP/s", "frac": round(tflops / peak_tf, 4)}}
@@ -345,8 +356,13 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev = torch.device("cuda", local_rank % torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("NTC_BENCH_BACKEND", "nccl")  # gloo: several ranks sharing one GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)

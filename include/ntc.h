@@ -114,6 +114,11 @@ ntc_status ntc_decode_texels(const ntc_material* m, const ntc_query* q, int64_t 
 ntc_status ntc_decode_mip(const ntc_material* m, int32_t mip, uint16_t* out, int64_t row_stride_elems,
                           ntc_stream stream);
 ntc_status ntc_decode_chain(const ntc_material* m, uint16_t* out, ntc_stream stream);
+/* Multi-GPU partition of ntc_decode_chain (multi-GPU): the chain's 128-texel tiles
+ * are split into nparts contiguous ranges of equal size; this call decodes range `part`
+ * into the same chain layout as ntc_decode_chain (other texels of out are not written).  */
+ntc_status ntc_decode_chain_part(const ntc_material* m, int32_t part, int32_t nparts, uint16_t* out,
+                                 ntc_stream stream);
 
 /* Tests only: runs the decode kernels' own addressing + input assembly for n queries and
  * writes addr device int32 [n][17] = {level, G0 taps (x,y) x4, G1 taps (x,y) x4} and
@@ -139,14 +144,18 @@ typedef struct {
 
 /* One batch = n_crops crops at one mip: crops host int32 [n_crops][4] =
  * (x0, y0, w, h), each inside the mip; ref device fp16 reference mip image,
- * row y at ref + y*ref_row_stride_elems (R24).  n_crops <= NTC_MAX_CROPS.              */
-#define NTC_MAX_CROPS 16
+ * row y at ref + y*ref_row_stride_elems (R24).  n_crops <= NTC_MAX_CROPS.
+ * norm_texels: the B of the mean over B*c values (R17); 0 = this batch's own texel count.
+ * A data-parallel rank passes the global batch's count so that the sum of the ranks'
+ * gradients is the global gradient.                                                     */
+#define NTC_MAX_CROPS 64
 typedef struct {
     int32_t mip;
     int32_t n_crops;
     const int32_t* crops;
     const uint16_t* ref;
     int64_t ref_row_stride_elems;
+    int64_t norm_texels;
 } ntc_batch;
 
 typedef struct {
@@ -179,10 +188,22 @@ ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const ntc_train_buf
 
 /* Footprint of a batch (host, pure): disjoint boxes (level, grid k, x0, y0, x1, y1) of
  * inclusive cell ranges that together cover exactly the grid cells read by the crops'
- * texels (at most 64 boxes; a pathological overlap pattern falls back to one bounding box
+ * texels (at most 256 boxes; a pathological overlap pattern falls back to one bounding box
  * per grid).  Returns the box count (-1 on a bad batch); pass boxes = NULL to query it,
  * otherwise boxes must hold [count][6] int32.                                            */
 int32_t ntc_train_footprint(const ntc_desc* d, const ntc_batch* batch, int32_t* boxes);
+
+/* Data-parallel latent-gradient exchange (multi-GPU): the latents inside the
+ * footprint of `batch` (normally the GLOBAL batch: every rank's crops) in box order.
+ * ntc_footprint_size: element count (host, pure; -1 on a bad batch).
+ * ntc_footprint_pack: packed[i] = src[latent of footprint element i] (device fp32).
+ * ntc_footprint_unpack: dst[latent of footprint element i] = packed[i], or 0 if packed is
+ *   NULL (zeroes the footprint).                                                          */
+int64_t ntc_footprint_size(const ntc_desc* d, const ntc_batch* batch);
+ntc_status ntc_footprint_pack(const ntc_desc* d, const ntc_batch* batch, const float* src, float* packed,
+                              ntc_stream stream);
+ntc_status ntc_footprint_unpack(const ntc_desc* d, const ntc_batch* batch, const float* packed, float* dst,
+                                ntc_stream stream);
 
 #ifdef __cplusplus
 }

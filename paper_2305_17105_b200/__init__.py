@@ -24,7 +24,7 @@ NTC_ERR_CUDA = 5
 NTC_ERR_UNSUPPORTED = 6
 NTC_STEP_GRADS = 1
 NTC_STEP_APPLY = 2
-NTC_MAX_CROPS = 16
+NTC_MAX_CROPS = 64
 
 
 class NtcError(RuntimeError):
@@ -45,7 +45,7 @@ class TrainBuffers(ctypes.Structure):
 
 class Batch(ctypes.Structure):
     _fields_ = [("mip", ctypes.c_int32), ("n_crops", ctypes.c_int32), ("crops", ctypes.c_void_p),
-                ("ref", ctypes.c_void_p), ("ref_row_stride_elems", ctypes.c_int64)]
+                ("ref", ctypes.c_void_p), ("ref_row_stride_elems", ctypes.c_int64), ("norm_texels", ctypes.c_int64)]
 
 
 class Hparams(ctypes.Structure):
@@ -73,6 +73,11 @@ ABI_FUNCTIONS = {
     "ntc_decode_mip": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
                                       ctypes.c_void_p]),
     "ntc_decode_chain": (ctypes.c_int, [ctypes.c_void_p] * 3),
+    "ntc_decode_chain_part": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                                             ctypes.c_void_p]),
+    "ntc_footprint_size": (ctypes.c_int64, [ctypes.c_void_p] * 2),
+    "ntc_footprint_pack": (ctypes.c_int, [ctypes.c_void_p] * 5),
+    "ntc_footprint_unpack": (ctypes.c_int, [ctypes.c_void_p] * 5),
     "ntc_debug_assemble": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p]),
     "ntc_trainer_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
@@ -226,6 +231,11 @@ def ntc_decode_chain(mat: Material, out: torch.Tensor, stream=None):
     _check(lib().ntc_decode_chain(mat.handle, _ptr(out), _stream(stream)))
 
 
+def ntc_decode_chain_part(mat: Material, part: int, nparts: int, out: torch.Tensor, stream=None):
+    assert out.dtype == torch.float16 and out.numel() >= ntc_chain_texels(mat.profile) * mat.desc.channels
+    _check(lib().ntc_decode_chain_part(mat.handle, part, nparts, _ptr(out), _stream(stream)))
+
+
 def ntc_debug_assemble(mat: Material, queries: torch.Tensor, addr: torch.Tensor, X: torch.Tensor, stream=None):
     _check(lib().ntc_debug_assemble(mat.handle, _ptr(queries), queries.numel(), _ptr(addr), _ptr(X),
                                     _stream(stream)))
@@ -252,12 +262,12 @@ class Trainer:
             pass
 
 
-def make_batch(mip: int, crops, ref: torch.Tensor, ref_row_stride_elems: int):
+def make_batch(mip: int, crops, ref: torch.Tensor, ref_row_stride_elems: int, norm_texels: int = 0):
     """crops: host int32 contiguous (n, 4) array-like (kept alive by the returned tuple)."""
     import numpy as np
 
     cr = np.ascontiguousarray(np.asarray(crops, dtype=np.int32).reshape(-1, 4))
-    b = Batch(mip, cr.shape[0], cr.ctypes.data_as(ctypes.c_void_p), _ptr(ref), ref_row_stride_elems)
+    b = Batch(mip, cr.shape[0], cr.ctypes.data_as(ctypes.c_void_p), _ptr(ref), ref_row_stride_elems, norm_texels)
     return b, cr
 
 
@@ -282,3 +292,24 @@ def ntc_train_footprint(d, batch):
     boxes = np.zeros((n, 6), np.int32)
     lib().ntc_train_footprint(ctypes.byref(make_desc(d)), ctypes.byref(b), boxes.ctypes.data_as(ctypes.c_void_p))
     return boxes
+
+
+def _b(batch):
+    return batch[0] if isinstance(batch, tuple) else batch
+
+
+def ntc_footprint_size(d, batch) -> int:
+    n = lib().ntc_footprint_size(ctypes.byref(make_desc(d)), ctypes.byref(_b(batch)))
+    if n < 0:
+        raise NtcError(NTC_ERR_INVALID_ARGUMENT, lib().ntc_last_error().decode())
+    return n
+
+
+def ntc_footprint_pack(d, batch, src: torch.Tensor, packed: torch.Tensor, stream=None):
+    _check(lib().ntc_footprint_pack(ctypes.byref(make_desc(d)), ctypes.byref(_b(batch)), _ptr(src), _ptr(packed),
+                                    _stream(stream)))
+
+
+def ntc_footprint_unpack(d, batch, packed, dst: torch.Tensor, stream=None):
+    _check(lib().ntc_footprint_unpack(ctypes.byref(make_desc(d)), ctypes.byref(_b(batch)), _ptr(packed), _ptr(dst),
+                                      _stream(stream)))

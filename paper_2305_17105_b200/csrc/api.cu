@@ -330,7 +330,8 @@ static int grid_for(const ntc_material* m, int64_t tiles) {
 }
 
 static ntc_status launch_tiles(const ntc_material* m, int mip_first, int mip_count, uint16_t* out,
-                               const int64_t* out_off, const int64_t* row_stride, cudaStream_t st) {
+                               const int64_t* out_off, const int64_t* row_stride, cudaStream_t st, int part = 0,
+                               int nparts = 1) {
     DecodeParams p = base_params(m);
     p.mode = 0;
     p.out = out;
@@ -347,7 +348,12 @@ static ntc_status launch_tiles(const ntc_material* m, int mip_first, int mip_cou
     for (int i = mip_count; i <= MAX_MIPS; ++i) p.tile_start[i] = INT32_MAX;
     p.tile_start[mip_count] = (int32_t)t;
     p.n_tiles = (int32_t)t;
-    cudaError_t e = launch_decode(m->pid, m->d.hidden_mats, p, grid_for(m, t), st);
+    // part of the tile range: [t*part/nparts, t*(part+1)/nparts)
+    const int64_t t0 = t * part / nparts, t1 = t * (part + 1) / nparts;
+    p.tile_first = (int32_t)t0;
+    p.n_tiles = (int32_t)t1;
+    if (t1 <= t0) return NTC_OK;
+    cudaError_t e = launch_decode(m->pid, m->d.hidden_mats, p, grid_for(m, t1 - t0), st);
     return e == cudaSuccess ? NTC_OK : cuda_fail(e, "decode_kernel");
 }
 
@@ -359,6 +365,18 @@ extern "C" ntc_status ntc_decode_chain(const ntc_material* m, uint16_t* out, ntc
         rs[mi] = (int64_t)(m->d.width >> mi) * m->d.channels;
     }
     return launch_tiles(m, 0, m->M, out, off, rs, (cudaStream_t)stream);
+}
+
+extern "C" ntc_status ntc_decode_chain_part(const ntc_material* m, int32_t part, int32_t nparts, uint16_t* out,
+                                            ntc_stream stream) {
+    if (!m || !out) return fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (nparts < 1 || part < 0 || part >= nparts) return fail(NTC_ERR_INVALID_ARGUMENT, "bad part/nparts");
+    int64_t off[MAX_MIPS], rs[MAX_MIPS];
+    for (int mi = 0; mi < m->M; ++mi) {
+        off[mi] = ntc_mip_offset(&m->d, mi) * m->d.channels;
+        rs[mi] = (int64_t)(m->d.width >> mi) * m->d.channels;
+    }
+    return launch_tiles(m, 0, m->M, out, off, rs, (cudaStream_t)stream, part, nparts);
 }
 
 extern "C" ntc_status ntc_decode_mip(const ntc_material* m, int32_t mip, uint16_t* out, int64_t row_stride_elems,

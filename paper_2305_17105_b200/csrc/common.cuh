@@ -53,7 +53,8 @@ struct DecodeParams {
     int32_t tile_start[MAX_MIPS + 1];
     int64_t out_off[MAX_MIPS];     // element offset of mip in out
     int64_t row_stride[MAX_MIPS];  // elements
-    int32_t n_tiles;
+    int32_t n_tiles;     // end of the tile range (exclusive)
+    int32_t tile_first;  // start of the tile range (multi-GPU part)
     // mode 1 / 2
     const ntc_query* q;
     int64_t nq;

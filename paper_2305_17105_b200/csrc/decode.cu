@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
     Ctx<P> cx[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-        cx[c].tile = ((int)blockIdx.x * NW + wg) * 2 + c;
+        cx[c].tile = (p.mode == 0 ? p.tile_first : 0) + ((int)blockIdx.x * NW + wg) * 2 + c;
         cx[c].phase = 0;
         cx[c].abuf = smem_u32(s_a + (wg * 2 + c) * S::ABUF);
         cx[c].tcol = tmem + (uint32_t)(wg * 128 + c * 64);

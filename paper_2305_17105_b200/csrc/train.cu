@@ -25,7 +25,7 @@
 
 namespace ntc {
 
-constexpr int MAX_BOXES = 64;
+constexpr int MAX_BOXES = 256;
 constexpr int TRAIN_WG = 2;  // warpgroups (independent tile pipelines) per CTA
 
 struct Box {        // inclusive cell ranges of one grid
@@ -856,6 +856,53 @@ static int32_t box_prefix(const std::vector<Box>& boxes, Box* dst, int32_t* star
     return (int32_t)acc;
 }
 
+// packed <-> dense copy over footprint boxes (data-parallel latent-gradient exchange)
+__global__ void footprint_copy_kernel(const __grid_constant__ PrepParams p, const float* __restrict__ src,
+                                      float* __restrict__ dst, int unpack) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.box_start[p.nbox]) return;
+    int b;
+    int64_t li;
+    box_locate(p.box, p.box_start, p.nbox, i, b, li);
+    if (unpack)
+        dst[li] = src ? src[i] : 0.0f;
+    else
+        dst[i] = src[li];
+}
+
+extern "C" int64_t ntc_footprint_size(const ntc_desc* d, const ntc_batch* batch) {
+    if (!d || check_batch(d, batch) != NTC_OK) return -1;
+    int64_t n = 0;
+    for (const Box& b : footprint(d, batch)) n += (int64_t)(b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1) * b.C;
+    return n;
+}
+
+static ntc_status footprint_copy(const ntc_desc* d, const ntc_batch* batch, const float* src, float* dst, int unpack,
+                                 ntc_stream stream) {
+    if (!d) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL desc");
+    if (ntc_status s = check_batch(d, batch)) return s;
+    if (!dst || (!unpack && !src)) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+    PrepParams pp;
+    memset(&pp, 0, sizeof pp);
+    const std::vector<Box> boxes = footprint(d, batch);
+    pp.nbox = (int32_t)boxes.size();
+    const int32_t n = box_prefix(boxes, pp.box, pp.box_start);
+    if (n == 0) return NTC_OK;
+    footprint_copy_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(pp, src, dst, unpack);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? NTC_OK : api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
+}
+
+extern "C" ntc_status ntc_footprint_pack(const ntc_desc* d, const ntc_batch* batch, const float* src, float* packed,
+                                         ntc_stream stream) {
+    return footprint_copy(d, batch, src, packed, 0, stream);
+}
+
+extern "C" ntc_status ntc_footprint_unpack(const ntc_desc* d, const ntc_batch* batch, const float* packed,
+                                           float* dst, ntc_stream stream) {
+    return footprint_copy(d, batch, packed, dst, 1, stream);
+}
+
 extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const ntc_train_buffers* buf,
                                      const ntc_batch* batch, const ntc_train_hparams* hp, float* loss,
                                      int32_t* status, uint32_t flags, ntc_stream stream) {
@@ -927,7 +974,8 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.n_tiles = (int32_t)tiles;
         tp.ref = batch->ref;
         tp.ref_stride = batch->ref_row_stride_elems;
-        tp.inv_bc = (float)(1.0 / ((double)B * d->channels));
+        const int64_t Bn = batch->norm_texels > 0 ? batch->norm_texels : B;
+        tp.inv_bc = (float)(1.0 / ((double)Bn * d->channels));
         tp.noisy = buf->noisy;
         tp.grad_lat = buf->grad_lat;
         tp.wimg = t->wimg;

@@ -1,0 +1,113 @@
+"""GPU checks of the multi-GPU partitioner and the data-parallel training step.  Two ranks
+share cuda:0 (this environment exposes one GPU) over a gloo group; the NCCL path is the same
+code with backend="nccl" (bench.py under torchrun)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2305_17105_b200 as ntc
+from paper_2305_17105_b200.synth import Profile
+from helpers import material_inputs
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8])
+def test_decode_chain_part_covers_chain(O, nparts):
+    """The union of the parts of ntc_decode_chain_part is bit-identical to ntc_decode_chain."""
+    d = Profile.named("ntc0.2", 512, 9)
+    codes, w = material_inputs(O, d, 5)
+    mat = ntc.Material(d, torch.from_numpy(codes).to(DEV), torch.from_numpy(w.view(np.int16)).to(DEV))
+    T = ntc.ntc_chain_texels(d)
+    full = torch.empty(T * 9, dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_chain(mat, full)
+    parts = torch.full((T * 9,), float("nan"), dtype=torch.float16, device=DEV)
+    for p in range(nparts):
+        ntc.ntc_decode_chain_part(mat, p, nparts, parts)
+    torch.cuda.synchronize()
+    assert torch.equal(full.view(torch.int16), parts.view(torch.int16))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _setup():
+    import oracle as O
+    from paper_2305_17105_b200.synth import (box_mip_chain_u8, gen_crops, gen_latents, gen_reference_u8,
+                                             gen_weights_f32, u8_to_f16_bits)
+
+    d = Profile.named("ntc0.2", 128, 8)
+    lat = gen_latents(1, O.num_latents(d))
+    par = gen_weights_f32(2, d.input_dim, 8)
+    ref = u8_to_f16_bits(box_mip_chain_u8(gen_reference_u8(3, 128, 8))[0])
+    gcrops = gen_crops(4, 128, 0, 5, 32)
+    return d, lat, par, ref, gcrops
+
+
+def _worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2305_17105_b200 as ntc
+        from paper_2305_17105_b200.dist import DataParallelTrainer
+
+        d, lat, par, ref, gcrops = _setup()
+        tr = DataParallelTrainer(d, torch.from_numpy(lat).to(DEV), torch.from_numpy(par).to(DEV))
+        refd = torch.from_numpy(ref.view(np.int16)).to(DEV)
+        hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, 1, 7, 1, 0)
+        loss = tr.step(0, gcrops, refd, 128 * 8, hp)
+        torch.cuda.synchronize()
+        q.put((rank, float(loss.item()), tr.t["grad_par"].cpu().numpy().copy(), tr.t["grad_lat"].cpu().numpy().copy(),
+               tr.t["params"].cpu().numpy().copy(), tr.t["latents"].cpu().numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dp_step_two_ranks_matches_single_batch():
+    """2-rank DP step == one GRADS+APPLY on the global batch: loss, all-reduced gradients
+    (fp32 summation order only) and identical replicas after the Adam step."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # single-process reference on the same GPU
+    d, lat, par, ref, gcrops = _setup()
+    NL, P = lat.size, par.size
+    t = {k: torch.zeros(NL, device=DEV) for k in ("m_lat", "v_lat", "grad_lat", "noisy")}
+    t.update({k: torch.zeros(P, device=DEV) for k in ("m_par", "v_par", "grad_par")})
+    t["latents"] = torch.from_numpy(lat.copy()).to(DEV)
+    t["params"] = torch.from_numpy(par.copy()).to(DEV)
+    refd = torch.from_numpy(ref.view(np.int16)).to(DEV)
+    loss = torch.zeros(1, device=DEV)
+    ntc.ntc_train_step(ntc.Trainer(d), ntc.make_buffers(t), ntc.make_batch(0, gcrops, refd, 128 * 8),
+                       ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, 1, 7, 1, 0), loss, flags=ntc.NTC_STEP_GRADS)
+    torch.cuda.synchronize()
+    gp, gl = t["grad_par"].cpu().numpy(), t["grad_lat"].cpu().numpy()
+    for r in res:
+        _, l, dgp, dgl, _, _ = r
+        assert abs(l - loss.item()) <= 1e-5 * loss.item()
+        assert np.linalg.norm(dgp - gp) <= 1e-5 * np.linalg.norm(gp)
+        assert np.linalg.norm(dgl - gl) <= 1e-5 * np.linalg.norm(gl)
+    assert np.array_equal(res[0][4], res[1][4]) and np.array_equal(res[0][5], res[1][5])
