@@ -139,7 +139,8 @@ ntc_status ntc_debug_assemble(const ntc_material* m, const ntc_query* q, int64_t
 typedef struct {
     float *latents, *m_lat, *v_lat, *grad_lat;
     float *params, *m_par, *v_par, *grad_par;
-    float* noisy; /* scratch: noisy latents, written inside the batch footprint only */
+    float* noisy; /* scratch (>= 2*num_latents bytes): fp16 noisy latents, written inside the
+                   * batch footprint only                                                   */
 } ntc_train_buffers;
 
 /* One batch = n_crops crops at one mip: crops host int32 [n_crops][4] =

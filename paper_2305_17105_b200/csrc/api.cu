@@ -193,6 +193,7 @@ struct ntc_material {
     uint4* wimg = nullptr;
     uint32_t wimg_bytes = 0;
     LevelGeom lv[MAX_LEVELS];
+    float b3[16];
     int num_sms = 148;
 };
 
@@ -268,7 +269,18 @@ extern "C" ntc_status ntc_material_create(const ntc_desc* d, const uint8_t* code
                 m->grids + (k ? m->lv[j].off1 : m->lv[j].off0));
         }
     e = build_wimg(m->pid, hm, weights_f16, d->channels, reinterpret_cast<uint8_t*>(m->wimg), st);
+    // the output bias b3 (last c parameters) travels as a kernel parameter
+    uint16_t hb3[16] = {0};
+    const int64_t P = ntc_num_params(d);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(hb3, weights_f16 + P - d->channels, sizeof(uint16_t) * d->channels,
+                            cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    for (int i = 0; i < 16; ++i) {
+        __half_raw r;
+        r.x = i < d->channels ? hb3[i] : 0;
+        m->b3[i] = __half2float(__half(r));
+    }
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
         ntc_material_destroy(m);
@@ -304,6 +316,7 @@ static DecodeParams base_params(const ntc_material* m) {
     p.M = m->M;
     p.L = m->L;
     for (int j = 0; j < m->L; ++j) p.lv[j] = m->lv[j];
+    memcpy(p.b3, m->b3, sizeof p.b3);
     for (int mi = 0; mi < m->M; ++mi) {
         p.level_of[mi] = (int8_t)ntc_level_of_mip(&m->d, mi);
         const double lod = m->M > 1 ? (double)mi / (double)(m->M - 1) : 0.0;  // R6

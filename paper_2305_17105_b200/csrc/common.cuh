@@ -62,6 +62,7 @@ struct DecodeParams {
     int32_t* dbg_addr;
     uint16_t* dbg_X;
     uint16_t* out;
+    float b3[16];                  // output bias, added in the output epilogue
 };
 
 }  // namespace ntc

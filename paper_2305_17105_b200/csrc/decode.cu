@@ -258,11 +258,12 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
             tc_fence_after();
             const bool last = layer == HM;
             const uint64_t dl = last ? d_w3 : d_w2 + (uint64_t)((layer * S::W2_BYTES) >> 4);
-            const uint64_t bias_atom = last ? (16 * 128) >> 4 : (64 * 128) >> 4;
             const uint32_t id = last ? ID16 : ID64;
 #pragma unroll
             for (int k = 0; k < 4; ++k) mma_f16_ss(C.tcol, C.adesc + 2 * k, dl + 2 * k, id, k > 0);
-            mma_f16_ss(C.tcol, d_ones, dl + bias_atom, id, 1);
+            // hidden-layer bias: one K=16 MMA against the ones tile; the output bias is
+            // added in the output epilogue (FADD.SAT, free with the clamp)
+            if (!last) mma_f16_ss(C.tcol, d_ones, dl + (uint64_t)((64 * 128) >> 4), id, 1);
             mma_commit(C.bar);
         }
     };
@@ -278,7 +279,8 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
         uint32_t o[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            o[k] = pack_half2(__saturatef(__uint_as_float(r[2 * k])), __saturatef(__uint_as_float(r[2 * k + 1])));
+            o[k] = pack_half2(__saturatef(__uint_as_float(r[2 * k]) + p.b3[2 * k]),
+                              __saturatef(__uint_as_float(r[2 * k + 1]) + p.b3[2 * k + 1]));
         store_output(p, C.dst, C.valid, C.bad, o);  // R13: clamp [0,1]
         tc_fence_before();
         C.tile += stride;

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -50,12 +51,13 @@ struct TrainParams {
     int64_t ref_stride;
     float inv_bc;
     // buffers
-    const float* noisy;
+    const __half* noisy;
     float* grad_lat;
     const uint8_t* wimg;  // fp16 weight image (TrainSmem layout, WEND bytes)
     float* partial;     // [grid * TRAIN_WG][P]
     float* loss_partial;  // [grid * TRAIN_WG]
     int32_t P;
+    int32_t debug_flags;  // profiling only (NTC_DEBUG_TRAIN env): 1 = skip the latent scatter
 };
 
 // ------------------------------------------------------------------ Philox noise (R16)
@@ -78,7 +80,7 @@ struct PrepParams {
     int32_t nbox;
     int32_t box_start[MAX_BOXES + 1];  // prefix of latents per box
     const float* latents;
-    float* noisy;
+    __half* noisy;  // fp16 noisy latents (the fp16 network-input format, R14)
     float* grad_lat;
     uint64_t seed;
     uint32_t step;
@@ -113,17 +115,19 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
         const float u = (float)(2u * (w >> 9) + 1u) * 5.9604644775390625e-8f;
         v += (u - 0.5f) * (1.0f / (float)(1 << p.box[b].bits));
     }
-    p.noisy[li] = v;
+    p.noisy[li] = __float2half_rn(v);
     p.grad_lat[li] = 0.0f;
 }
 
 // ------------------------------------------------------------------ fused forward + backward
 struct TrainSmem {
-    static constexpr uint32_t W1 = 0, W2 = 8192, W2B = 16384, W3 = 24576, W3B = 26624, WEND = 28672;
+    // fp16 weight images (W1 with b1 at column D, W2, W3) + fp32 biases b2[64], b3[16]
+    static constexpr uint32_t W1 = 0, W2 = 8192, W3 = 16384, BIAS = 18432, WEND = 19456;
     static constexpr uint32_t TILE = 128 * 128;  // one 128 x 64 fp16 SW128 tile
     enum { X = 0, H1 = 1, H2 = 2, G1 = 3, G2 = 4, D3 = 5, NT = 6 };
     static constexpr uint32_t WG_BYTES = NT * TILE;
-    static constexpr uint32_t BYTES = 1024 + WEND + TRAIN_WG * WG_BYTES + 256;
+    static constexpr uint32_t MISC = 256 + 16 * NTC_MAX_CROPS + 4 * (NTC_MAX_CROPS + 1) + 12;
+    static constexpr uint32_t BYTES = 1024 + WEND + TRAIN_WG * WG_BYTES + MISC;
 };
 
 __device__ __forceinline__ void sts_row_chunk(uint32_t tile, int row, int chunk, uint32_t a, uint32_t b, uint32_t c,
@@ -153,13 +157,22 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 
 __device__ __forceinline__ uint32_t h2u(float a, float b) { return pack_half2(a, b); }
 
-// fp16 SW128 weight image of the current fp32 master weights (t3): W1 (+ b1 at column D),
-// W2, b2 at column D of a bias atom (it multiplies X's constant 1), W3 (16 rows), b3 atom
+// fp16 SW128 weight image of the current fp32 master weights (t3): W1 (+ b1 at column D, it
+// multiplies X's constant 1), W2, W3 (16 rows); b2 and b3 as fp32 values of their fp16 rounding
+// (R14), added in the epilogues
 __global__ void train_wimg_kernel(const float* __restrict__ w, int D, int c, uint8_t* __restrict__ img) {
     using S = TrainSmem;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 5 * 4096) return;
     const int P1 = D * HID;
+    if (i >= 3 * 4096) {
+        const int j = i - 3 * 4096;
+        if (j < HID)
+            reinterpret_cast<float*>(img + S::BIAS)[j] = __half2float(__float2half_rn(w[P1 + HID + HID * HID + j]));
+        else if (j < HID + 16)
+            reinterpret_cast<float*>(img + S::BIAS)[j] =
+                (j - HID) < c ? __half2float(__float2half_rn(w[P1 + 2 * HID + HID * HID + HID * c + (j - HID)])) : 0.0f;
+        return;
+    }
     const int part = i / 4096, e = i % 4096, r = e / 64, k = e % 64;
     float v = 0.0f;
     uint32_t base;
@@ -169,17 +182,10 @@ __global__ void train_wimg_kernel(const float* __restrict__ w, int D, int c, uin
     } else if (part == 1) {
         v = w[P1 + HID + r * HID + k];
         base = S::W2;
-    } else if (part == 2) {
-        v = k == D ? w[P1 + HID + HID * HID + r] : 0.0f;
-        base = S::W2B;
-    } else if (part == 3) {
+    } else {
         if (r >= 16) return;
         v = r < c ? w[P1 + HID + HID * HID + HID + r * HID + k] : 0.0f;
         base = S::W3;
-    } else {
-        if (r >= 16) return;
-        v = (r < c && k == D) ? w[P1 + 2 * HID + HID * HID + HID * c + r] : 0.0f;
-        base = S::W3B;
     }
     *reinterpret_cast<__half*>(img + base + sw128_offset(r, k)) = __float2half_rn(v);
 }
@@ -189,14 +195,15 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     using S = TrainSmem;
     constexpr int D = 4 * C0 + C1 + 13;
     constexpr int NLAT = 4 * C0 + C1;   // latent columns of X
-    constexpr int KB = D / 16;          // k-step of X holding the constant-1 column D
     static_assert(D < 64 && NLAT <= 48, "training kernel: K1 = 64 profiles");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::WEND + TRAIN_WG * S::WG_BYTES);
-    float* s_loss = reinterpret_cast<float*>(s_bar + TRAIN_WG);
+    float* s_loss = reinterpret_cast<float*>(s_bar + 2 * TRAIN_WG);
     uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_loss + 4);
     uint32_t* s_tmem = s_pe + 32;
+    int4* s_crop = reinterpret_cast<int4*>(s_tmem + 4);
+    int* s_ts = reinterpret_cast<int*>(s_crop + NTC_MAX_CROPS);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wg = warp >> 2, q = warp & 3, row = q * 32 + lane;
@@ -208,8 +215,10 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.wimg) + i);
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
     if (tid < 4) s_loss[tid] = 0.0f;
+    if (tid < NTC_MAX_CROPS) s_crop[tid] = make_int4(p.crop[tid][0], p.crop[tid][1], p.crop[tid][2], p.crop[tid][3]);
+    if (tid <= NTC_MAX_CROPS) s_ts[tid] = p.tile_start[tid];
     if (tid == 0) {
-        for (int i = 0; i < TRAIN_WG; ++i) mbar_init(&s_bar[i], 1);
+        for (int i = 0; i < 2 * TRAIN_WG; ++i) mbar_init(&s_bar[i], 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -231,7 +240,9 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     const uint32_t tG1 = tiles + S::G1 * S::TILE, tG2 = tiles + S::G2 * S::TILE, tD3 = tiles + S::D3 * S::TILE;
     const bool issuer = q == 0 && lane == 0;
     uint64_t* bar = &s_bar[wg];
-    uint32_t phase = 0;
+    uint64_t* bar2 = &s_bar[TRAIN_WG + wg];
+    uint32_t phase = 0, phase2 = 0;
+    bool pending_w = false;  // weight-gradient MMAs of the previous tile in flight
     auto sync_wg = [&]() {
         fence_proxy_async_smem();
         tc_fence_before();
@@ -243,8 +254,8 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         tc_fence_after();
     };
     const uint64_t dW1 = umma_desc_k_sw128(sbase + S::W1), dW2 = umma_desc_k_sw128(sbase + S::W2);
-    const uint64_t dW2B = umma_desc_k_sw128(sbase + S::W2B), dW3 = umma_desc_k_sw128(sbase + S::W3);
-    const uint64_t dW3B = umma_desc_k_sw128(sbase + S::W3B);
+    const uint64_t dW3 = umma_desc_k_sw128(sbase + S::W3);
+    const float* s_bias = reinterpret_cast<const float*>(smem + S::BIAS);  // b2[64], b3[16]
     const uint64_t dX = umma_desc_k_sw128(tX), dH1 = umma_desc_k_sw128(tH1), dH2 = umma_desc_k_sw128(tH2);
     const uint64_t dG1 = umma_desc_k_sw128(tG1), dG2 = umma_desc_k_sw128(tG2), dD3 = umma_desc_k_sw128(tD3);
     // MN-major views: W^T operands and the stacked [X^T; H1^T], [X^T; H2^T], delta^T tiles
@@ -261,94 +272,138 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     bool first = true;
     const int lw = p.lw;
 
-    for (int tile = blockIdx.x * TRAIN_WG + wg; tile < p.n_tiles; tile += gridDim.x * TRAIN_WG) {
-        // ---- t1: texel of this row
+    // ---- t1/a1: texel of `row` in `tile`, its taps (same integer addressing as decode, R1-R3)
+    struct Texel {
+        int x, y;
+        bool valid;
+    };
+    auto texel_of = [&](int tile) {
         int k = 0;
-        while (tile >= p.tile_start[k + 1]) ++k;
-        const int cw = p.crop[k][2], chh = p.crop[k][3];
-        const int li = (tile - p.tile_start[k]) * TILE_M + row;
-        const bool valid = li < cw * chh;
-        const int x = p.crop[k][0] + (valid ? li % cw : 0), y = p.crop[k][1] + (valid ? li / cw : 0);
-        // ---- a1: taps (same integer addressing as decode, R1-R3)
+        while (tile >= s_ts[k + 1]) ++k;
+        const int4 cr = s_crop[k];
+        const int li = (tile - s_ts[k]) * TILE_M + row;
+        Texel t;
+        t.valid = li < cr.z * cr.w;
+        t.x = cr.x + (t.valid ? li % cr.z : 0);
+        t.y = cr.y + (t.valid ? li / cr.z : 0);
+        return t;
+    };
+    auto taps_of = [&](const Texel& t, int (&tx0)[2], int (&ty0)[2], int (&tx1)[2], int (&ty1)[2], uint32_t (&wq)[4]) {
+        const int xs = 2 * t.x + 1, ys = 2 * t.y + 1;
+        int nx = (xs << p.lr0) - (1 << lw), ny = (ys << p.lr0) - (1 << lw);
+        int i = nx >> (lw + 1), j = ny >> (lw + 1);
+        tx0[0] = max(i, 0);
+        tx0[1] = min(i + 1, p.r0 - 1);
+        ty0[0] = max(j, 0);
+        ty0[1] = min(j + 1, p.r0 - 1);
+        nx = (xs << p.lr1) - (1 << lw);
+        ny = (ys << p.lr1) - (1 << lw);
+        i = nx >> (lw + 1);
+        j = ny >> (lw + 1);
+        const int mask = (2 << lw) - 1;  // bilinear weights in 1/256 units (exact, see decode)
+        const uint32_t ax = (uint32_t)(((nx & mask) << 4) >> (lw + 1)), ay = (uint32_t)(((ny & mask) << 4) >> (lw + 1));
+        wq[0] = (16u - ax) * (16u - ay);
+        wq[1] = ax * (16u - ay);
+        wq[2] = (16u - ax) * ay;
+        wq[3] = ax * ay;
+        tx1[0] = max(i, 0);
+        tx1[1] = min(i + 1, p.r1 - 1);
+        ty1[0] = max(j, 0);
+        ty1[1] = min(j + 1, p.r1 - 1);
+    };
+    // ---- t2 fetch of one texel: fp16 noisy latents of the 8 taps + raw reference, issued one
+    // tile ahead so the loads overlap the previous tile's MMA chain
+    static_assert(C0 == 8 && C1 % 4 == 0, "fetch layout: 16-byte G0 cells, 8-byte-aligned G1 cells");
+    struct Fetch {
+        Texel t;
+        uint4 g0[4];
+        uint2 g1[4][C1 / 4];
+        uint32_t wq[4];
+        uint32_t ref[8];
+    };
+    auto fetch = [&](int tile, Fetch& f) {
+        f.t = texel_of(tile);
         int tx0[2], ty0[2], tx1[2], ty1[2];
-        float wt[4];
-        {
-            const int xs = 2 * x + 1, ys = 2 * y + 1;
-            int nx = (xs << p.lr0) - (1 << lw), ny = (ys << p.lr0) - (1 << lw);
-            int i = nx >> (lw + 1), j = ny >> (lw + 1);
-            tx0[0] = max(i, 0);
-            tx0[1] = min(i + 1, p.r0 - 1);
-            ty0[0] = max(j, 0);
-            ty0[1] = min(j + 1, p.r0 - 1);
-            nx = (xs << p.lr1) - (1 << lw);
-            ny = (ys << p.lr1) - (1 << lw);
-            i = nx >> (lw + 1);
-            j = ny >> (lw + 1);
-            const int mask = (2 << lw) - 1;
-            const float ax = (float)(nx & mask) / (float)(2 << lw), ay = (float)(ny & mask) / (float)(2 << lw);
-            wt[0] = (1.0f - ax) * (1.0f - ay);
-            wt[1] = ax * (1.0f - ay);
-            wt[2] = (1.0f - ax) * ay;
-            wt[3] = ax * ay;
-            tx1[0] = max(i, 0);
-            tx1[1] = min(i + 1, p.r1 - 1);
-            ty1[0] = max(j, 0);
-            ty1[1] = min(j + 1, p.r1 - 1);
+        taps_of(f.t, tx0, ty0, tx1, ty1, f.wq);
+        const __half* g0 = p.noisy + p.off0;
+        const __half* g1 = p.noisy + p.off1;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            f.g0[t] = __ldg(reinterpret_cast<const uint4*>(g0 + (ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0));
+            const uint2* c1 = reinterpret_cast<const uint2*>(g1 + (ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1);
+#pragma unroll
+            for (int e = 0; e < C1 / 4; ++e) f.g1[t][e] = __ldg(c1 + e);
         }
-        const float* g0 = p.noisy + p.off0;
-        const float* g1 = p.noisy + p.off1;
-        // ---- t2/a2-a4: X row (canonical column order, R4) -> SW128 tile
+        const uint16_t* rp = p.ref + (int64_t)f.t.y * p.ref_stride + (int64_t)f.t.x * c;
+#pragma unroll
+        for (int o = 0; o < 8; ++o) {
+            uint16_t lo = 0, hi = 0;
+            if (2 * o < c) lo = __ldg(rp + 2 * o);
+            if (2 * o + 1 < c) hi = __ldg(rp + 2 * o + 1);
+            f.ref[o] = (uint32_t)lo | ((uint32_t)hi << 16);
+        }
+    };
+
+    int tile = blockIdx.x * TRAIN_WG + wg;
+    const int tstride = gridDim.x * TRAIN_WG;
+    Fetch F;
+    if (tile < p.n_tiles) fetch(tile, F);
+    for (; tile < p.n_tiles; tile += tstride) {
+        const Texel T = F.t;
+        const bool valid = T.valid;
+        uint32_t rawref[8];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) rawref[o] = F.ref[o];
+        // ---- a2-a4: X row (canonical column order, R4) -> SW128 tile
         {
             uint32_t xw[32];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const float* cp = g0 + ((int64_t)ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0;
-#pragma unroll
-                for (int e = 0; e < C0; e += 4) {
-                    const float4 v = *reinterpret_cast<const float4*>(cp + e);
-                    xw[(t * C0 + e) / 2] = h2u(v.x, v.y);
-                    xw[(t * C0 + e) / 2 + 1] = h2u(v.z, v.w);
-                }
+            for (int t = 0; t < 4; ++t) {  // G0 taps: the fp16 noisy latents are X
+                xw[4 * t + 0] = F.g0[t].x;
+                xw[4 * t + 1] = F.g0[t].y;
+                xw[4 * t + 2] = F.g0[t].z;
+                xw[4 * t + 3] = F.g0[t].w;
             }
-            {
+            {  // G1 bilinear in fp32 from the fp16 taps, rounded once
                 float acc[C1];
 #pragma unroll
                 for (int e = 0; e < C1; ++e) acc[e] = 0.0f;
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const float* cp = g1 + ((int64_t)ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1;
+                    const float wf = (float)F.wq[t] * (1.0f / 256.0f);
 #pragma unroll
-                    for (int e = 0; e < C1; e += 4) {
-                        const float4 v = *reinterpret_cast<const float4*>(cp + e);
-                        acc[e] = fmaf(wt[t], v.x, acc[e]);
-                        acc[e + 1] = fmaf(wt[t], v.y, acc[e + 1]);
-                        acc[e + 2] = fmaf(wt[t], v.z, acc[e + 2]);
-                        acc[e + 3] = fmaf(wt[t], v.w, acc[e + 3]);
+                    for (int e = 0; e < C1 / 4; ++e) {
+                        const uint2 v = F.g1[t][e];
+                        const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+                        const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+                        acc[4 * e + 0] = fmaf(wf, a0.x, acc[4 * e + 0]);
+                        acc[4 * e + 1] = fmaf(wf, a0.y, acc[4 * e + 1]);
+                        acc[4 * e + 2] = fmaf(wf, a1.x, acc[4 * e + 2]);
+                        acc[4 * e + 3] = fmaf(wf, a1.y, acc[4 * e + 3]);
                     }
                 }
 #pragma unroll
                 for (int e = 0; e < C1; e += 2) xw[(4 * C0 + e) / 2] = h2u(acc[e], acc[e + 1]);
             }
+            if (pending_w) {  // the previous tile's weight-gradient MMAs still read the tiles
+                mbar_wait(bar2, phase2);
+                phase2 ^= 1;
+                tc_fence_after();
+                pending_w = false;
+            }
             constexpr int PEW = NLAT / 2;
-            xw[PEW + 0] = s_pe[4 * (x & 7) + 0];
-            xw[PEW + 1] = s_pe[4 * (x & 7) + 1];
-            xw[PEW + 2] = s_pe[4 * (x & 7) + 2];
-            xw[PEW + 3] = s_pe[4 * (y & 7) + 0];
-            xw[PEW + 4] = s_pe[4 * (y & 7) + 1];
-            xw[PEW + 5] = s_pe[4 * (y & 7) + 2];
+            xw[PEW + 0] = s_pe[4 * (T.x & 7) + 0];
+            xw[PEW + 1] = s_pe[4 * (T.x & 7) + 1];
+            xw[PEW + 2] = s_pe[4 * (T.x & 7) + 2];
+            xw[PEW + 3] = s_pe[4 * (T.y & 7) + 0];
+            xw[PEW + 4] = s_pe[4 * (T.y & 7) + 1];
+            xw[PEW + 5] = s_pe[4 * (T.y & 7) + 2];
             xw[PEW + 6] = p.lod_word;
 #pragma unroll
             for (int e = PEW + 7; e < 32; ++e) xw[e] = 0u;
 #pragma unroll
             for (int ch = 0; ch < 8; ++ch)
                 sts_row_chunk(tX, row, ch, xw[4 * ch], xw[4 * ch + 1], xw[4 * ch + 2], xw[4 * ch + 3]);
-        }
-        // reference texel (R24: fp16 of v/255 prepared by the caller)
-        float ref[16];
-        {
-            const uint16_t* rp = p.ref + (int64_t)y * p.ref_stride + (int64_t)x * c;
-#pragma unroll
-            for (int o = 0; o < 16; ++o) ref[o] = o < c ? __half2float(__ushort_as_half(rp[o])) : 0.0f;
         }
         sync_wg();
         // ---- t3: forward.  Z1 = X W1^T (+b1)
@@ -358,8 +413,9 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
             for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dX + 2 * kk, dW1 + 2 * kk, ID64, kk > 0);
             mma_commit(bar);
         }
+        if (tile + tstride < p.n_tiles) fetch(tile + tstride, F);  // next tile's loads in flight
         wait_mma();
-        auto hidden_epilogue = [&](uint32_t tH, uint32_t tG) {
+        auto hidden_epilogue = [&](uint32_t tH, uint32_t tG, bool bias) {
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 uint32_t r[32];
@@ -368,7 +424,12 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
                 uint32_t h[16], g[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    const float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
+                    float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
+                    if (bias) {
+                        const float2 bb = *reinterpret_cast<const float2*>(s_bias + 32 * half + 2 * i);
+                        z0 += bb.x;
+                        z1 += bb.y;
+                    }
                     h[i] = h2u(hgelu(z0), hgelu(z1));
                     g[i] = h2u(hgelu_d(z0), hgelu_d(z1));
                 }
@@ -379,25 +440,23 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
                 }
             }
         };
-        hidden_epilogue(tH1, tG1);
+        hidden_epilogue(tH1, tG1, false);
         sync_wg();
         // Z2 = H1 W2^T + b2 (bias through X's constant column)
         if (issuer) {
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH1 + 2 * kk, dW2 + 2 * kk, ID64, kk > 0);
-            mma_f16_ss(t_s, dX + 2 * KB, dW2B + 2 * KB, ID64, 1);
             mma_commit(bar);
         }
         wait_mma();
-        hidden_epilogue(tH2, tG2);
+        hidden_epilogue(tH2, tG2, true);
         sync_wg();
         // Y = H2 W3^T + b3
         if (issuer) {
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH2 + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
-            mma_f16_ss(t_s, dX + 2 * KB, dW3B + 2 * KB, ID16, 1);
             mma_commit(bar);
         }
         wait_mma();
@@ -409,7 +468,10 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
             float d3[16];
 #pragma unroll
             for (int o = 0; o < 16; ++o) {
-                const float e = (valid && o < c) ? __uint_as_float(r[o]) - ref[o] : 0.0f;
+                float rf;
+                asm volatile("{\n\t.reg .f16 h;\n\tmov.b16 h, %1;\n\tcvt.f32.f16 %0, h;\n\t}" : "=f"(rf)
+                             : "h"((uint16_t)(rawref[o >> 1] >> (16 * (o & 1)))));
+                const float e = (valid && o < c) ? __uint_as_float(r[o]) + s_bias[HID + o] - rf : 0.0f;
                 loss_acc = fmaf(e, e, loss_acc);
                 d3[o] = 2.0f * e;
             }
@@ -422,10 +484,6 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         if (issuer) {
             tc_fence_after();
             mma_f16_ss(t_s, dD3, mW3, ID64_BT, 0);
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-                mma_f16_ss(t_acc_b, mXH2 + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
-                           (!first || kk > 0) ? 1u : 0u);
             mma_commit(bar);
         }
         wait_mma();
@@ -459,10 +517,6 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
                 mma_f16_ss(t_s, dG2 + 2 * kk, mW2 + (uint64_t)(kk * 128), ID64_BT, kk > 0);
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-                mma_f16_ss(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
-                           (!first || kk > 0) ? 1u : 0u);
             mma_commit(bar);
         }
         wait_mma();
@@ -474,14 +528,26 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
                 mma_f16_ss(t_s, dG1 + 2 * kk, mW1 + (uint64_t)(kk * 128), ID48_BT, kk > 0);
+            mma_commit(bar);
+            // weight gradients, off the critical path: they run while this tile scatters and
+            // the next tile fetches; bar2 is waited before the next tile overwrites the tiles
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                mma_f16_ss(t_acc_b, mXH2 + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
+                           (!first || kk > 0) ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                mma_f16_ss(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
+                           (!first || kk > 0) ? 1u : 0u);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
                 mma_f16_ss(t_acc_a, mXH1 + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID64_AB,
                            (!first || kk > 0) ? 1u : 0u);
-            mma_commit(bar);
+            mma_commit(bar2);
         }
         wait_mma();
         first = false;
+        pending_w = true;
         // ---- t7: latent-gradient scatter: G0 taps unweighted, G1 taps bilinear-weighted
         {
             uint32_t r[48];
@@ -495,28 +561,88 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
 #pragma unroll
                 for (int i = 0; i < 16; ++i) r[32 + i] = b[i];
             }
-            if (valid) {
-                const float s = p.inv_bc;
-                float* gl0 = p.grad_lat + p.off0;
-                float* gl1 = p.grad_lat + p.off1;
+            // Pre-reduce in the warp: neighbouring texels share tap cells (runs of 4 texels
+            // share all four G0 cells and runs of 8 share the G1 cells at LOD 0), so each run
+            // is summed to its first lane with two (G0) / three (G1) shuffle steps and only run
+            // heads issue the vector reductions -- no global contention storm.
+            int tx0[2], ty0[2], tx1[2], ty1[2];
+            uint32_t wq[4];
+            taps_of(T, tx0, ty0, tx1, ty1, wq);
+            const float s = p.inv_bc;
+            float* gl0 = p.grad_lat + p.off0;
+            float* gl1 = p.grad_lat + p.off1;
+            const bool on = valid && !(p.debug_flags & 1);
+            // run keys (invalid lanes get unique keys and never merge)
+            const uint32_t kx0 = on ? (uint32_t)(tx0[0] | (tx0[1] << 16)) : 0xFFFFFFF0u - lane;
+            const uint32_t ky0 = (uint32_t)(ty0[0] | (ty0[1] << 16));
+            const uint32_t kx1 = on ? (uint32_t)(tx1[0] | (tx1[1] << 16)) : 0xFFFFFFF0u - lane;
+            const uint32_t ky1 = (uint32_t)T.y;  // same y => same y-weights within a G1 run
+            const uint32_t ky1b = (uint32_t)(ty1[0] | (ty1[1] << 16));
+            // G0: 32 values (tap-major), unweighted
+            float g0v[32];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    float* dst = gl0 + ((int64_t)ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0;
+            for (int i = 0; i < 32; ++i) g0v[i] = on ? __uint_as_float(r[i]) : 0.0f;
+            // G1: per x-tap a, S_a = sum over the run of wx_a * dX_G1 (wy is constant in a run)
+            const float ax = (float)(wq[1] + wq[3]) * (1.0f / 256.0f);  // x-weight of tap column 1
+            const float ay = (float)(wq[2] + wq[3]) * (1.0f / 256.0f);  // y-weight of tap row 1
+            float g1v[2 * C1];
 #pragma unroll
-                    for (int e = 0; e < C0; e += 4)
-                        red_add_v4(dst + e, s * __uint_as_float(r[t * C0 + e]), s * __uint_as_float(r[t * C0 + e + 1]),
-                                   s * __uint_as_float(r[t * C0 + e + 2]), s * __uint_as_float(r[t * C0 + e + 3]));
+            for (int e = 0; e < C1; ++e) {
+                const float v = on ? __uint_as_float(r[4 * C0 + e]) : 0.0f;
+                g1v[e] = (1.0f - ax) * v;
+                g1v[C1 + e] = ax * v;
+            }
+#pragma unroll
+            for (int d = 1; d <= 4; d <<= 1) {
+                const uint32_t nx0 = __shfl_down_sync(0xffffffffu, kx0, d), ny0 = __shfl_down_sync(0xffffffffu, ky0, d);
+                const uint32_t nx1 = __shfl_down_sync(0xffffffffu, kx1, d), ny1 = __shfl_down_sync(0xffffffffu, ky1, d);
+                const uint32_t ny1b = __shfl_down_sync(0xffffffffu, ky1b, d);
+                const bool in = lane + d < 32;
+                const bool s0 = in && nx0 == kx0 && ny0 == ky0 && d < 4;
+                const bool s1 = in && nx1 == kx1 && ny1 == ky1 && ny1b == ky1b;
+                if (d < 4) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float o = __shfl_down_sync(0xffffffffu, g0v[i], d);
+                        if (s0) g0v[i] += o;
+                    }
                 }
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    float* dst = gl1 + ((int64_t)ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1;
-                    const float sw = s * wt[t];
-                    if (sw != 0.0f) {
+                for (int i = 0; i < 2 * C1; ++i) {
+                    const float o = __shfl_down_sync(0xffffffffu, g1v[i], d);
+                    if (s1) g1v[i] += o;
+                }
+            }
+            const uint32_t px0 = __shfl_up_sync(0xffffffffu, kx0, 1), py0 = __shfl_up_sync(0xffffffffu, ky0, 1);
+            const uint32_t px1 = __shfl_up_sync(0xffffffffu, kx1, 1), py1 = __shfl_up_sync(0xffffffffu, ky1, 1);
+            const uint32_t py1b = __shfl_up_sync(0xffffffffu, ky1b, 1);
+            // run heads; runs never exceed 4 (G0) / 8 (G1) lanes since r0/w_m >= 1/4 and
+            // r1/w_m >= 1/8 for the compiled profiles, which the 2 / 3 steps cover
+            const bool head1 = lane == 0 || px1 != kx1 || py1 != ky1 || py1b != ky1b;
+            if (on) {
+                const bool h0 = lane == 0 || px0 != kx0 || py0 != ky0;
+                if (h0) {
 #pragma unroll
-                        for (int e = 0; e < C1; e += 4)
-                            red_add_v4(dst + e, sw * __uint_as_float(r[4 * C0 + e]),
-                                       sw * __uint_as_float(r[4 * C0 + e + 1]), sw * __uint_as_float(r[4 * C0 + e + 2]),
-                                       sw * __uint_as_float(r[4 * C0 + e + 3]));
+                    for (int t = 0; t < 4; ++t) {
+                        float* dst = gl0 + ((int64_t)ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0;
+#pragma unroll
+                        for (int e = 0; e < C0; e += 4)
+                            red_add_v4(dst + e, s * g0v[t * C0 + e], s * g0v[t * C0 + e + 1], s * g0v[t * C0 + e + 2],
+                                       s * g0v[t * C0 + e + 3]);
+                    }
+                }
+                if (head1) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float wy = (t >> 1) ? ay : 1.0f - ay;
+                        const float* S = g1v + (t & 1) * C1;
+                        float* dst = gl1 + ((int64_t)ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1;
+                        const float sw = s * wy;
+                        if (sw != 0.0f) {
+#pragma unroll
+                            for (int e = 0; e < C1; e += 4)
+                                red_add_v4(dst + e, sw * S[e], sw * S[e + 1], sw * S[e + 2], sw * S[e + 3]);
+                        }
                     }
                 }
             }
@@ -524,6 +650,11 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         tc_fence_before();
     }
 
+    if (pending_w) {
+        mbar_wait(bar2, phase2);
+        phase2 ^= 1;
+        tc_fence_after();
+    }
     // ---- t6: this warpgroup's weight-gradient partial (unscaled) + loss partial
     float* part = p.partial + (size_t)(blockIdx.x * TRAIN_WG + wg) * p.P;
     {
@@ -923,7 +1054,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         pp.nbox = (int32_t)boxes.size();
         const int32_t n = box_prefix(boxes, pp.box, pp.box_start);
         pp.latents = buf->latents;
-        pp.noisy = buf->noisy;
+        pp.noisy = reinterpret_cast<__half*>(buf->noisy);
         pp.grad_lat = buf->grad_lat;
         pp.seed = hp->seed;
         pp.step = (uint32_t)hp->step;
@@ -976,14 +1107,15 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.ref_stride = batch->ref_row_stride_elems;
         const int64_t Bn = batch->norm_texels > 0 ? batch->norm_texels : B;
         tp.inv_bc = (float)(1.0 / ((double)Bn * d->channels));
-        tp.noisy = buf->noisy;
+        tp.noisy = reinterpret_cast<const __half*>(buf->noisy);
         tp.grad_lat = buf->grad_lat;
         tp.wimg = t->wimg;
-        train_wimg_kernel<<<(5 * 4096 + 255) / 256, 256, 0, st>>>(buf->params, 4 * d->c0 + d->c1 + 13, d->channels,
+        train_wimg_kernel<<<(3 * 4096 + 80 + 255) / 256, 256, 0, st>>>(buf->params, 4 * d->c0 + d->c1 + 13, d->channels,
                                                                  t->wimg);
         tp.partial = t->partial;
         tp.loss_partial = t->loss_partial;
         tp.P = (int32_t)P;
+        if (const char* dbg = getenv("NTC_DEBUG_TRAIN")) tp.debug_flags = atoi(dbg);
         const int grid = (int)std::min<int64_t>(t->num_sms, (tiles + TRAIN_WG - 1) / TRAIN_WG);
         auto* k = train_kernel<8, 12>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TrainSmem::BYTES);
