@@ -655,45 +655,61 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         phase2 ^= 1;
         tc_fence_after();
     }
-    // ---- t6: this warpgroup's weight-gradient partial (unscaled) + loss partial
-    float* part = p.partial + (size_t)(blockIdx.x * TRAIN_WG + wg) * p.P;
-    {
-        const int P1 = D * HID, o2 = P1 + HID, o3 = o2 + HID * HID + HID;
-        const int m = row;  // stacked rows: [0,64) X features, [64,128) H units
-        if (first) {  // no tile processed: zero partial
-            for (int i = row; i < p.P; i += 128) part[i] = 0.0f;
-        } else {
+    // ---- t6: the CTA's weight-gradient partial (unscaled, one per CTA, fixed order): warpgroup
+    // 1 parks its TMEM accumulators in the (now idle) SMEM tile area, warpgroup 0 adds its own
+    // and writes the partial
+    float* part = p.partial + (size_t)blockIdx.x * p.P;
+    float* park = reinterpret_cast<float*>(smem + S::WEND) + row * 145;  // [128][144] (+1 pad)
+    auto read_acc = [&](float (&v)[144], bool have) {
 #pragma unroll
-            for (int blk = 0; blk < 4; ++blk) {
-                uint32_t r[32];
-                tmem_ld32(t_acc_a + lane_off + 32 * blk, r);
-                tmem_wait_ld();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int col = 32 * blk + e;
-                    const float v = __uint_as_float(r[e]);
-                    if (m < 64) {
-                        if (col < 64) {
-                            if (m < D) part[col * D + m] = v;          // dW1[j][i]
-                            else if (m == D) part[P1 + col] = v;       // db1[j]
-                        } else if (m == D) {
-                            part[o2 + HID * HID + (col - 64)] = v;     // db2[j]
-                        }
-                    } else if (col >= 64) {
-                        part[o2 + (col - 64) * HID + (m - 64)] = v;    // dW2[j][i]
-                    }
-                }
-            }
-            uint32_t r[16];
-            tmem_ld16(t_acc_b + lane_off, r);
+        for (int blk = 0; blk < 4; ++blk) {
+            uint32_t r[32];
+            tmem_ld32(t_acc_a + lane_off + 32 * blk, r);
             tmem_wait_ld();
 #pragma unroll
-            for (int o = 0; o < 16; ++o) {
-                if (o >= c) continue;
-                const float v = __uint_as_float(r[o]);
-                if (m == D) part[o3 + HID * c + o] = v;                // db3[o]
-                else if (m >= 64) part[o3 + o * HID + (m - 64)] = v;   // dW3[o][i]
+            for (int e = 0; e < 32; ++e) v[32 * blk + e] = have ? __uint_as_float(r[e]) : 0.0f;
+        }
+        uint32_t r[16];
+        tmem_ld16(t_acc_b + lane_off, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int o = 0; o < 16; ++o) v[128 + o] = have ? __uint_as_float(r[o]) : 0.0f;
+    };
+    __syncthreads();  // both warpgroups are done with their tiles before the area is reused
+    if (wg == 1) {
+        float v[144];
+        read_acc(v, !first);
+#pragma unroll
+        for (int e = 0; e < 144; ++e) park[e] = v[e];
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (wg == 0) {
+        float v[144];
+        read_acc(v, !first);
+#pragma unroll
+        for (int e = 0; e < 144; ++e) v[e] += park[e];
+        const int P1 = D * HID, o2 = P1 + HID, o3 = o2 + HID * HID + HID;
+        const int m = row;  // stacked rows: [0,64) X features, [64,128) H units
+#pragma unroll
+        for (int col = 0; col < 128; ++col) {
+            if (m < 64) {
+                if (col < 64) {
+                    if (m < D) part[col * D + m] = v[col];           // dW1[j][i]
+                    else if (m == D) part[P1 + col] = v[col];        // db1[j]
+                } else if (m == D) {
+                    part[o2 + HID * HID + (col - 64)] = v[col];      // db2[j]
+                }
+            } else if (col >= 64) {
+                part[o2 + (col - 64) * HID + (m - 64)] = v[col];     // dW2[j][i]
             }
+        }
+#pragma unroll
+        for (int o = 0; o < 16; ++o) {
+            if (o >= c) continue;
+            if (m == D) part[o3 + HID * c + o] = v[128 + o];                // db3[o]
+            else if (m >= 64) part[o3 + o * HID + (m - 64)] = v[128 + o];   // dW3[o][i]
         }
     }
     {
@@ -709,19 +725,27 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     if (warp == 0) tmem_dealloc(*s_tmem, 512);
 }
 
-// fixed-order reduction of the partials (deterministic), scaled by 1/(B c): block = 32
-// parameters x 8 partial groups; group g sums partials g, g+8, ...; the 8 group sums are
-// then added in order.
-__global__ void reduce_kernel(const float* __restrict__ partial, const float* __restrict__ loss_partial, int nparts,
-                              int P, float inv_bc, float* __restrict__ grad, float* __restrict__ loss,
+// fixed-order reduction of the per-CTA partials (deterministic), scaled by 1/(B c): block =
+// 32 parameters x 8 partial groups; group g sums partials g, g+8, ... (four independent
+// accumulators, combined in a fixed order); the 8 group sums are then added in order.
+__global__ void reduce_kernel(const float* __restrict__ partial, size_t part_stride, const float* __restrict__ loss_partial,
+                              int nparts, int P, float inv_bc, float* __restrict__ grad, float* __restrict__ loss,
                               int32_t* __restrict__ status) {
     __shared__ float s[8][33];
     const int px = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int i = blockIdx.x * 32 + px;
-    float acc = 0.0f;
-    if (i < P)
-        for (int w = g; w < nparts; w += 8) acc += __ldg(partial + (size_t)w * P + i);
-    s[g][px] = acc;
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    if (i < P) {
+        int w = g;
+        for (; w + 24 < nparts; w += 32) {
+            a0 += __ldg(partial + (size_t)w * part_stride + i);
+            a1 += __ldg(partial + (size_t)(w + 8) * part_stride + i);
+            a2 += __ldg(partial + (size_t)(w + 16) * part_stride + i);
+            a3 += __ldg(partial + (size_t)(w + 24) * part_stride + i);
+        }
+        for (; w < nparts; w += 8) a0 += __ldg(partial + (size_t)w * part_stride + i);
+    }
+    s[g][px] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     if (g == 0 && i < P) {
         float t = 0.0f;
@@ -731,7 +755,7 @@ __global__ void reduce_kernel(const float* __restrict__ partial, const float* __
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         float t = 0.0f;
-        for (int w = 0; w < nparts; ++w) t += loss_partial[w];
+        for (int w = 0; w < nparts * TRAIN_WG; ++w) t += loss_partial[w];
         const float l = t * inv_bc;
         *loss = l;
         if (!isfinite(l) && status) atomicOr(status, (int)NTC_ERR_NONFINITE);
@@ -1122,8 +1146,8 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         if (e == cudaSuccess) {
             k<<<grid, TRAIN_WG * 128, TrainSmem::BYTES, st>>>(tp);
             // t6: deterministic cross-CTA reduction, scaled by 1/(B c)
-            reduce_kernel<<<(int)((P + 31) / 32), 256, 0, st>>>(t->partial, t->loss_partial, grid * TRAIN_WG,
-                                                                   (int)P, tp.inv_bc, buf->grad_par, loss, status);
+            reduce_kernel<<<(int)((P + 31) / 32), 256, 0, st>>>(t->partial, (size_t)P, t->loss_partial,
+                                                                 grid, (int)P, tp.inv_bc, buf->grad_par, loss, status);
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
