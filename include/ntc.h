@@ -83,6 +83,9 @@ int64_t ntc_mip_offset(const ntc_desc* d, int32_t mip); /* texel offset of mip i
  * B = b0 for G0 grids, b1 for G1 grids (R9, R10).  Bit-exact.
  * latents: device fp32 [num_latents]; codes: device uint8 [num_latents].                  */
 ntc_status ntc_quantize_latents(const ntc_desc* d, const float* latents, uint8_t* codes, ntc_stream stream);
+/* latents[i] = (codes[i] - (N/2 - 1)) Q: the bin centres.  Used to freeze the
+ * explicitly quantised latents for the weight-only finetune.               */
+ntc_status ntc_dequantize_codes(const ntc_desc* d, const uint8_t* codes, float* latents, ntc_stream stream);
 
 /* ---------------------------------------------------------------- material (decode side)
  * codes: device uint8 [num_latents], canonical layout, each < 2^B of its grid.
@@ -166,6 +169,9 @@ typedef struct {
     uint64_t seed;
     int32_t noise_on;           /* 1: simulated quantisation noise             */
     int32_t dense_latent_adam;  /* 0: footprint-sparse Adam, skip g == 0 (R18); 1: dense      */
+    int32_t freeze_latents;     /* 1: frozen phase: latents are held at their
+                                 * quantised values -- GRADS skips the latent-gradient scatter,
+                                 * APPLY updates only the weights; use with noise_on = 0      */
 } ntc_train_hparams;
 
 enum { NTC_STEP_GRADS = 1, NTC_STEP_APPLY = 2 };

@@ -51,7 +51,8 @@ class Batch(ctypes.Structure):
 class Hparams(ctypes.Structure):
     _fields_ = [("lr_latent", ctypes.c_float), ("lr_weight", ctypes.c_float), ("beta1", ctypes.c_float),
                 ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("step", ctypes.c_int32),
-                ("seed", ctypes.c_uint64), ("noise_on", ctypes.c_int32), ("dense_latent_adam", ctypes.c_int32)]
+                ("seed", ctypes.c_uint64), ("noise_on", ctypes.c_int32), ("dense_latent_adam", ctypes.c_int32),
+                ("freeze_latents", ctypes.c_int32)]
 
 
 ABI_FUNCTIONS = {
@@ -66,6 +67,7 @@ ABI_FUNCTIONS = {
     "ntc_chain_texels": (ctypes.c_int64, [ctypes.c_void_p]),
     "ntc_mip_offset": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int32]),
     "ntc_quantize_latents": (ctypes.c_int, [ctypes.c_void_p] * 4),
+    "ntc_dequantize_codes": (ctypes.c_int, [ctypes.c_void_p] * 4),
     "ntc_material_create": (ctypes.c_int, [ctypes.c_void_p] * 5),
     "ntc_material_destroy": (None, [ctypes.c_void_p]),
     "ntc_decode_texels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
@@ -178,6 +180,11 @@ def grid_list(d):
 def ntc_quantize_latents(d, latents: torch.Tensor, codes: torch.Tensor, stream=None):
     assert latents.is_cuda and latents.dtype == torch.float32 and codes.dtype == torch.uint8
     _check(lib().ntc_quantize_latents(ctypes.byref(make_desc(d)), _ptr(latents), _ptr(codes), _stream(stream)))
+
+
+def ntc_dequantize_codes(d, codes: torch.Tensor, latents: torch.Tensor, stream=None):
+    assert codes.dtype == torch.uint8 and latents.dtype == torch.float32
+    _check(lib().ntc_dequantize_codes(ctypes.byref(make_desc(d)), _ptr(codes), _ptr(latents), _stream(stream)))
 
 
 # ---------------------------------------------------------------- material + decode

@@ -185,6 +185,26 @@ extern "C" ntc_status ntc_quantize_latents(const ntc_desc* d, const float* laten
     return e == cudaSuccess ? NTC_OK : cuda_fail(e, "quantize_kernel");
 }
 
+__global__ void dequantize_kernel(const uint8_t* __restrict__ codes, float* __restrict__ lat, const GridTable t) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= t.start[t.n]) return;
+    int g = 0;
+    while (i >= t.start[g + 1]) ++g;
+    const int N = 1 << t.bits[g];
+    lat[i] = (float)((int)codes[i] - (N / 2 - 1)) / (float)N;
+}
+
+extern "C" ntc_status ntc_dequantize_codes(const ntc_desc* d, const uint8_t* codes, float* latents,
+                                           ntc_stream stream) {
+    if (ntc_status s = check_desc(d)) return s;
+    if (!latents || !codes) return fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+    const GridTable t = grid_table(d);
+    const int64_t n = t.start[t.n];
+    dequantize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(codes, latents, t);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? NTC_OK : cuda_fail(e, "dequantize_kernel");
+}
+
 // ------------------------------------------------------------------ material
 struct ntc_material {
     ntc_desc d;

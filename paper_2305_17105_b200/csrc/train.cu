@@ -58,6 +58,7 @@ struct TrainParams {
     float* loss_partial;  // [grid * TRAIN_WG]
     int32_t P;
     int32_t debug_flags;  // profiling only (NTC_DEBUG_TRAIN env): 1 = skip the latent scatter
+    int32_t freeze;       // frozen phase: no latent gradients
 };
 
 // ------------------------------------------------------------------ Philox noise (R16)
@@ -571,7 +572,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
             const float s = p.inv_bc;
             float* gl0 = p.grad_lat + p.off0;
             float* gl1 = p.grad_lat + p.off1;
-            const bool on = valid && !(p.debug_flags & 1);
+            const bool on = valid && !(p.debug_flags & 1) && !p.freeze;
             // run keys (invalid lanes get unique keys and never merge)
             const uint32_t kx0 = on ? (uint32_t)(tx0[0] | (tx0[1] << 16)) : 0xFFFFFFF0u - lane;
             const uint32_t ky0 = (uint32_t)(ty0[0] | (ty0[1] << 16));
@@ -779,6 +780,7 @@ struct AdamParams {
     float* v_lat;
     const float* grad_lat;
     float lr_w, lr_l, b1, b2, eps, c1, c2;  // c1 = 1 - b1^t, c2 = 1 - b2^t
+    int32_t freeze;                         // skip the latents (frozen phase)
     // dense-latent mode: per-grid bits lookup
     int32_t ngrid;
     int64_t grid_start[2 * MAX_LEVELS + 1];
@@ -802,6 +804,7 @@ __global__ void adam_kernel(const __grid_constant__ AdamParams a) {
         return;
     }
     const int64_t j = i - a.P;
+    if (a.freeze) return;
     int64_t li;
     int bits;
     if (a.dense_latents) {
@@ -1140,6 +1143,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.loss_partial = t->loss_partial;
         tp.P = (int32_t)P;
         if (const char* dbg = getenv("NTC_DEBUG_TRAIN")) tp.debug_flags = atoi(dbg);
+        tp.freeze = hp->freeze_latents;
         const int grid = (int)std::min<int64_t>(t->num_sms, (tiles + TRAIN_WG - 1) / TRAIN_WG);
         auto* k = train_kernel<8, 12>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TrainSmem::BYTES);
@@ -1173,6 +1177,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         a.grad_lat = buf->grad_lat;
         a.lr_w = hp->lr_weight;
         a.lr_l = hp->lr_latent;
+        a.freeze = hp->freeze_latents;
         a.b1 = hp->beta1;
         a.b2 = hp->beta2;
         a.eps = hp->eps;
@@ -1192,7 +1197,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
             acc = o1 + (int64_t)r1 * r1 * d->c1;
         }
         a.grid_start[2 * L] = acc;
-        const int64_t total = P + (hp->dense_latent_adam ? NL : (int64_t)n);
+        const int64_t total = P + (hp->freeze_latents ? 0 : (hp->dense_latent_adam ? NL : (int64_t)n));
         adam_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
         e = cudaGetLastError();
         if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
