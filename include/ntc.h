@@ -123,6 +123,22 @@ ntc_status ntc_decode_chain(const ntc_material* m, uint16_t* out, ntc_stream str
 ntc_status ntc_decode_chain_part(const ntc_material* m, int32_t part, int32_t nparts, uint16_t* out,
                                  ntc_stream stream);
 
+/* Texture filtering on top of random-access decode.
+ * uvl: device fp32 [n][3] = (u, v, lod): u, v in [0,1) (texel x of mip m has centre
+ * (x + 1/2)/w_m), lod >= 0.  mode:
+ *   0 nearest: mip floor(lod + 1/2), texel floor(u w_m) (clamped);
+ *   1 bilinear: 4 decodes at mip floor(lod + 1/2), clamp-to-edge;
+ *   2 trilinear: 8 decodes, mips floor(lod) and floor(lod)+1 blended by frac(lod);
+ *   3 stochastic bilinear: (u, v) jittered by U(-1/2, 1/2) texel, then nearest -- 1 decode
+ *     (PAPER.md:631-633); 4 stochastic trilinear: LOD jittered by U(-1/2, 1/2) too.
+ *   Jitter: Philox4x32-10, key = seed, ctr = (i, i >> 32, 0, 'FILT'), words 0/1/2 ->
+ *   (2(w >> 9) + 1) 2^-24 - 1/2.
+ * out: device fp16 [n][c]; scratch: device, ntc_filter_scratch_bytes(n, mode, c) bytes
+ * (query list, blend weights, tap decodes).  Each decode is clamped to [0,1] (R13).       */
+int64_t ntc_filter_scratch_bytes(int64_t n, int32_t mode, int32_t channels);
+ntc_status ntc_filter_texels(const ntc_material* m, const float* uvl, int64_t n, int32_t mode, uint64_t seed,
+                             uint16_t* out, void* scratch, ntc_stream stream);
+
 /* Tests only: runs the decode kernels' own addressing + input assembly for n queries and
  * writes addr device int32 [n][17] = {level, G0 taps (x,y) x4, G1 taps (x,y) x4} and
  * X device uint16 [n][D] (fp16 network input, R4).  Out-of-range queries are

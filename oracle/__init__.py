@@ -81,6 +81,7 @@ def lib():
             "ntco_decode_texels": (None, [P(Desc), vp, vp, vp, i64, vp, i32]),
             "ntco_decode_mip": (None, [P(Desc), vp, vp, i32, vp, i32]),
             "ntco_philox4x32_10": (None, [vp, vp, vp]),
+            "ntco_filter": (None, [P(Desc), vp, vp, vp, i64, i32, u64, vp, i32]),
             "ntco_noise": (f64, [u64, ctypes.c_uint32, i64, i32]),
             "ntco_train_grads": (
                 f64,
@@ -240,6 +241,18 @@ def decode_mip(d, codes, weights_f16, m, nthreads: int = 0) -> np.ndarray:
     w = np.ascontiguousarray(weights_f16, np.uint16)
     out = np.zeros((wm, wm, dd.channels), np.float64)
     lib().ntco_decode_mip(ctypes.byref(dd), _p(codes), _p(w), m, _p(out), nthreads)
+    return out
+
+
+def filter_texels(d, codes, weights_f16, uvl, mode, seed=0, nthreads=0) -> np.ndarray:
+    """uvl: (n, 3) float64 (u, v, lod); mode 0 nearest, 1 bilinear, 2 trilinear, 3 stochastic
+    bilinear, 4 stochastic trilinear.  Returns (n, c) float64."""
+    dd = desc_from(d)
+    q = np.ascontiguousarray(uvl, np.float64)
+    codes = np.ascontiguousarray(codes, np.uint8)
+    w = np.ascontiguousarray(weights_f16, np.uint16)
+    out = np.zeros((q.shape[0], dd.channels), np.float64)
+    lib().ntco_filter(ctypes.byref(dd), _p(codes), _p(w), _p(q), q.shape[0], mode, seed, _p(out), nthreads)
     return out
 
 

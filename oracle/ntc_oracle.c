@@ -356,6 +356,67 @@ void ntco_decode_mip(const ntco_desc* d, const uint8_t* codes, const uint16_t* w
 }
 
 /* ------------------------------------------------------------------------- */
+/* Filtering                                               */
+/* ------------------------------------------------------------------------- */
+static double jitter_word(uint32_t w) { return ldexp((double)(2 * (w >> 9) + 1), -24) - 0.5; }
+
+/* bilinear filter of mip m at texture coordinate (u, v): texel centres at (i + 1/2)/w_m,
+ * clamp-to-edge (the same convention as the latent grids, R1-R2)                    */
+static void bilinear_at(const ntco_desc* d, const uint8_t* codes, const double* params, int32_t m, double u,
+                        double v, double* out) {
+    int32_t wm = d->width >> m;
+    double s = u * wm - 0.5, t = v * wm - 0.5;
+    double fs = floor(s), ft = floor(t);
+    double a = s - fs, b = t - ft;
+    int32_t i = (int32_t)fs, j = (int32_t)ft;
+    double w[4] = {(1 - a) * (1 - b), a * (1 - b), (1 - a) * b, a * b};
+    double y[16];
+    for (int32_t c = 0; c < d->channels; ++c) out[c] = 0.0;
+    for (int32_t k = 0; k < 4; ++k) {
+        int32_t x = clampi(i + (k & 1), 0, wm - 1), yy = clampi(j + (k >> 1), 0, wm - 1);
+        decode_one(d, codes, params, x, yy, m, y);
+        for (int32_t c = 0; c < d->channels; ++c) out[c] += w[k] * y[c];
+    }
+}
+
+void ntco_filter(const ntco_desc* d, const uint8_t* codes, const uint16_t* weights_f16, const double* uvl,
+                 int64_t n, int32_t mode, uint64_t seed, double* out, int32_t nthreads) {
+    double* params = params_from_f16(d, weights_f16);
+    int32_t M = ntco_num_mips(d->width);
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t i = 0; i < n; ++i) {
+        double u = uvl[3 * i], v = uvl[3 * i + 1], lod = uvl[3 * i + 2];
+        double* o = out + i * d->channels;
+        uint32_t ctr[4] = {(uint32_t)i, (uint32_t)((uint64_t)i >> 32), 0u, 0x46494C54u /* 'FILT' */};
+        uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+        uint32_t r[4];
+        ntco_philox4x32_10(ctr, key, r);
+        if (mode == 4) lod += jitter_word(r[2]);
+        if (mode == 0 || mode == 3 || mode == 4) {
+            int32_t m = clampi((int32_t)floor(lod + 0.5), 0, M - 1), wm = d->width >> m;
+            double su = u * wm, sv = v * wm;
+            if (mode != 0) { su += jitter_word(r[0]); sv += jitter_word(r[1]); }
+            decode_one(d, codes, params, clampi((int32_t)floor(su), 0, wm - 1), clampi((int32_t)floor(sv), 0, wm - 1),
+                       m, o);
+        } else if (mode == 1) {
+            bilinear_at(d, codes, params, clampi((int32_t)floor(lod + 0.5), 0, M - 1), u, v, o);
+        } else {
+            double fl = floor(lod);
+            int32_t m0 = clampi((int32_t)fl, 0, M - 1), m1 = clampi(m0 + 1, 0, M - 1);
+            double t = (lod >= M - 1) ? 0.0 : (lod < 0 ? 0.0 : lod - fl);
+            double y0[16], y1[16];
+            bilinear_at(d, codes, params, m0, u, v, y0);
+            bilinear_at(d, codes, params, m1, u, v, y1);
+            for (int32_t c = 0; c < d->channels; ++c) o[c] = (1 - t) * y0[c] + t * y1[c];
+        }
+    }
+    free(params);
+}
+
+/* ------------------------------------------------------------------------- */
 /* Training                                                                   */
 /* ------------------------------------------------------------------------- */
 /* Philox4x32-10 (Salmon et al., SC'11), the counter-based generator both sides implement. */

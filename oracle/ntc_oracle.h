@@ -84,6 +84,15 @@ void ntco_decode_texels(const ntco_desc* d, const uint8_t* codes, const uint16_t
 void ntco_decode_mip(const ntco_desc* d, const uint8_t* codes, const uint16_t* weights_f16,
                      int32_t mip, double* out, int32_t nthreads);
 
+/* ---- filtering on top of random-access decode ----
+ * uvl: n x (u, v, lod) doubles, u, v in [0,1) texture coordinates, lod >= 0.
+ * mode 0 nearest (mip floor(lod+1/2)), 1 bilinear (4 decodes), 2 trilinear (8 decodes),
+ * 3 stochastic bilinear (U(-1/2,1/2) texel jitter, 1 decode), 4 stochastic trilinear
+ * (+ U(-1/2,1/2) LOD jitter).  Jitter: Philox4x32-10 key = seed, ctr = (i, i>>32, 0,
+ * 'FILT'), words 0/1/2 -> (2(w>>9)+1) 2^-24 - 1/2.  out: n x c doubles.                 */
+void ntco_filter(const ntco_desc* d, const uint8_t* codes, const uint16_t* weights_f16, const double* uvl,
+                 int64_t n, int32_t mode, uint64_t seed, double* out, int32_t nthreads);
+
 /* ---- training ---- */
 void   ntco_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 double ntco_noise(uint64_t seed, uint32_t step, int64_t latent_index, int32_t bits);

@@ -78,6 +78,9 @@ ABI_FUNCTIONS = {
     "ntc_decode_chain_part": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
                                              ctypes.c_void_p]),
     "ntc_footprint_size": (ctypes.c_int64, [ctypes.c_void_p] * 2),
+    "ntc_filter_scratch_bytes": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),
+    "ntc_filter_texels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                         ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ntc_footprint_pack": (ctypes.c_int, [ctypes.c_void_p] * 5),
     "ntc_footprint_unpack": (ctypes.c_int, [ctypes.c_void_p] * 5),
     "ntc_debug_assemble": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
@@ -236,6 +239,21 @@ def ntc_decode_mip(mat: Material, mip: int, out: torch.Tensor, row_stride_elems:
 def ntc_decode_chain(mat: Material, out: torch.Tensor, stream=None):
     assert out.dtype == torch.float16 and out.numel() >= ntc_chain_texels(mat.profile) * mat.desc.channels
     _check(lib().ntc_decode_chain(mat.handle, _ptr(out), _stream(stream)))
+
+
+NTC_FILTER_NEAREST, NTC_FILTER_BILINEAR, NTC_FILTER_TRILINEAR = 0, 1, 2
+NTC_FILTER_STOCHASTIC_BILINEAR, NTC_FILTER_STOCHASTIC_TRILINEAR = 3, 4
+
+
+def ntc_filter_texels(mat: Material, uvl: torch.Tensor, mode: int, out: torch.Tensor, seed: int = 0,
+                      scratch: torch.Tensor = None, stream=None):
+    """uvl: device fp32 (n, 3) = (u, v, lod); out: device fp16 (n, c)."""
+    assert uvl.dtype == torch.float32 and out.dtype == torch.float16
+    n = uvl.shape[0]
+    if scratch is None:
+        nb = lib().ntc_filter_scratch_bytes(n, mode, mat.desc.channels)
+        scratch = torch.empty(max(nb, 256), dtype=torch.uint8, device=uvl.device)
+    _check(lib().ntc_filter_texels(mat.handle, _ptr(uvl), n, mode, seed, _ptr(out), _ptr(scratch), _stream(stream)))
 
 
 def ntc_decode_chain_part(mat: Material, part: int, nparts: int, out: torch.Tensor, stream=None):

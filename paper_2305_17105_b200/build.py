@@ -20,7 +20,7 @@ def sources():
 
 
 def deps():
-    return sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [
+    return sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(os.path.join(HERE, "csrc", "*.h")) + [
         os.path.join(os.path.dirname(HERE), "include", "ntc.h")
     ]
 

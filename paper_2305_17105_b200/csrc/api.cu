@@ -206,16 +206,7 @@ extern "C" ntc_status ntc_dequantize_codes(const ntc_desc* d, const uint8_t* cod
 }
 
 // ------------------------------------------------------------------ material
-struct ntc_material {
-    ntc_desc d;
-    int pid, M, L;
-    uint8_t* grids = nullptr;
-    uint4* wimg = nullptr;
-    uint32_t wimg_bytes = 0;
-    LevelGeom lv[MAX_LEVELS];
-    float b3[16];
-    int num_sms = 148;
-};
+#include "material.h"
 
 // pack C codes (B bits each, LSB first) of one cell into CELL bytes
 __global__ void pack_kernel(const uint8_t* __restrict__ codes, int64_t src_off, int64_t ncells, int C, int B,
@@ -325,7 +316,13 @@ uint16_t host_f16(double v) { return float_to_half_bits(v); }
 double host_tri(double t) { return tri_wave(t); }
 }  // namespace ntc
 
-static DecodeParams base_params(const ntc_material* m) {
+namespace ntc {
+DecodeParams base_params(const ntc_material* m);
+cudaError_t decode_queries(const ntc_material* m, const ntc_query* q, int64_t n, uint16_t* out, int32_t* status,
+                           cudaStream_t s);
+}  // namespace ntc
+
+DecodeParams ntc::base_params(const ntc_material* m) {
     DecodeParams p;
     memset(&p, 0, sizeof p);
     p.grids = m->grids;
@@ -422,20 +419,24 @@ extern "C" ntc_status ntc_decode_mip(const ntc_material* m, int32_t mip, uint16_
     return launch_tiles(m, mip, 1, out, &off, &row_stride_elems, (cudaStream_t)stream);
 }
 
-extern "C" ntc_status ntc_decode_texels(const ntc_material* m, const ntc_query* q, int64_t n, uint16_t* out,
-                                        int32_t* status, ntc_stream stream) {
-    if (!m) return fail(NTC_ERR_INVALID_ARGUMENT, "NULL material");
-    if (n < 0) return fail(NTC_ERR_INVALID_ARGUMENT, "n < 0");
-    if (n == 0) return NTC_OK;
-    if (!q || !out) return fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+cudaError_t ntc::decode_queries(const ntc_material* m, const ntc_query* q, int64_t n, uint16_t* out, int32_t* status,
+                                cudaStream_t s) {
     DecodeParams p = base_params(m);
     p.mode = 1;
     p.q = q;
     p.nq = n;
     p.out = out;
     p.status = status;
-    cudaError_t e = launch_decode(m->pid, m->d.hidden_mats, p, grid_for(m, (n + TILE_M - 1) / TILE_M),
-                                  (cudaStream_t)stream);
+    return launch_decode(m->pid, m->d.hidden_mats, p, grid_for(m, (n + TILE_M - 1) / TILE_M), s);
+}
+
+extern "C" ntc_status ntc_decode_texels(const ntc_material* m, const ntc_query* q, int64_t n, uint16_t* out,
+                                        int32_t* status, ntc_stream stream) {
+    if (!m) return fail(NTC_ERR_INVALID_ARGUMENT, "NULL material");
+    if (n < 0) return fail(NTC_ERR_INVALID_ARGUMENT, "n < 0");
+    if (n == 0) return NTC_OK;
+    if (!q || !out) return fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+    cudaError_t e = decode_queries(m, q, n, out, status, (cudaStream_t)stream);
     return e == cudaSuccess ? NTC_OK : cuda_fail(e, "decode_kernel(queries)");
 }
 
