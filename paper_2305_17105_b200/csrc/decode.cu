@@ -147,6 +147,7 @@ struct Ctx {
     uint32_t abuf, tcol;
     uint64_t* bar;
     int id;             // context index (named barrier selector)
+    int iq;             // warp (lane quarter) that issues this context's MMAs
     uint64_t adesc;     // SW128 K-major descriptor of abuf
 };
 
@@ -192,15 +193,16 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
     // descriptors advance by (bytes >> 4) in their low 14-bit start-address field
     const uint64_t d_w1 = umma_desc_k_sw128(w1), d_w2 = umma_desc_k_sw128(w2), d_w3 = umma_desc_k_sw128(w3);
     const uint64_t d_ones = umma_desc_k_sw128(smem_u32(s_ones));
-    const bool issuer = (q == 0) && (lane == 0);
-    // Operand hand-off to the MMA issuer: warps 1-3 of the warpgroup only arrive on the
-    // context's named barrier (bar.arrive) and move on to the other context; warp 0 waits
-    // (bar.sync) and issues.  One barrier id per context keeps successive phases apart.
-    auto handoff = [&](int c) {
-        if (q == 0)
-            named_bar_sync(1 + wg * 2 + c, 128);
+    // Operand hand-off to the MMA issuer: three warps of the warpgroup only arrive on the
+    // context's named barrier (bar.arrive) and move on to the other context; the issuing
+    // warp waits (bar.sync) and issues.  One barrier id per context keeps successive phases
+    // apart.  The issuing warp rotates with (warpgroup, context) so the MMA-issue work is
+    // spread over the four SM sub-partitions instead of piling up on warp 0's.
+    auto handoff = [&](const Ctx<P>& C) {
+        if (q == C.iq)
+            named_bar_sync(1 + wg * 2 + C.id, 128);
         else
-            named_bar_arrive(1 + wg * 2 + c, 128);
+            named_bar_arrive(1 + wg * 2 + C.id, 128);
     };
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
     const int ntiles = p.mode == 0 ? p.n_tiles : (int)((p.nq + TILE_M - 1) / TILE_M);
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
         cx[c].tcol = tmem + (uint32_t)(wg * 128 + c * 64);
         cx[c].bar = &s_bar[wg * 2 + c];
         cx[c].id = c;
+        cx[c].iq = (wg * 2 + c) & 3;
         cx[c].adesc = umma_desc_k_sw128(cx[c].abuf);
         if (cx[c].tile < ntiles) fetch_tile<P>(p, cx[c].tile, row, cx[c].nxt);
     }
@@ -232,8 +235,8 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
         C.bad = C.nxt.bad;
         fence_proxy_async_smem();
         tc_fence_before();
-        handoff(C.id);
-        if (issuer) {
+        handoff(C);
+        if (q == C.iq && lane == 0) {
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < P::K1 / 16; ++k)
@@ -253,8 +256,8 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
         epilogue_hidden(C.tcol + lane_off, C.abuf, row);
         fence_proxy_async_smem();
         tc_fence_before();
-        handoff(C.id);
-        if (issuer) {
+        handoff(C);
+        if (q == C.iq && lane == 0) {
             tc_fence_after();
             const bool last = layer == HM;
             const uint64_t dl = last ? d_w3 : d_w2 + (uint64_t)((layer * S::W2_BYTES) >> 4);

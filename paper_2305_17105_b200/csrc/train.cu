@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     const uint32_t tiles = sbase + S::WEND + (uint32_t)wg * S::WG_BYTES;
     const uint32_t tX = tiles + S::X * S::TILE, tH1 = tiles + S::H1 * S::TILE, tH2 = tiles + S::H2 * S::TILE;
     const uint32_t tG1 = tiles + S::G1 * S::TILE, tG2 = tiles + S::G2 * S::TILE, tD3 = tiles + S::D3 * S::TILE;
-    const bool issuer = q == 0 && lane == 0;
+    const bool issuer = q == ((wg * 2) & 3) && lane == 0;  // issuing warps on different SM sub-partitions
     uint64_t* bar = &s_bar[wg];
     uint64_t* bar2 = &s_bar[TRAIN_WG + wg];
     uint32_t phase = 0, phase2 = 0;
