@@ -227,7 +227,7 @@ def run_ours(args, rank, world, local_rank):
                      "frac": round(achieved / peak_tf, 4), "traffic": tr_bytes,
                      "peak_source": f"{pk_src} bf16 dense burst (fp16 same rate)",
                      "kernel": "ntc::decode_kernel", "flops_per_texel": decode_flops_per_texel(d)},
-        "gpu_launches": args.steps * (1 + (0 if train is None else (5 if world == 1 else 8))),
+        "gpu_launches": args.steps * (1 + (0 if train is None else (4 if world == 1 else 7))),
         "clocks": clk.report(),
     })
     if train is not None:

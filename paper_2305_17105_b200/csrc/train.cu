@@ -86,6 +86,11 @@ struct PrepParams {
     uint64_t seed;
     uint32_t step;
     int32_t noise_on;
+    // fp16 weight image of the master weights, built by the trailing blocks of the same launch
+    int32_t prep_blocks;  // blocks [0, prep_blocks) do t2; the rest build the image
+    const float* params;
+    int32_t D, c;
+    uint8_t* wimg;
 };
 
 __device__ __forceinline__ void box_locate(const Box* box, const int32_t* start, int nbox, int32_t i, int& b,
@@ -97,27 +102,6 @@ __device__ __forceinline__ void box_locate(const Box* box, const int32_t* start,
     const int32_t w = (B.x1 - B.x0 + 1) * B.C;
     const int32_t yy = B.y0 + k / w, rem = k % w;
     li = B.off + ((int64_t)yy * B.r + B.x0) * B.C + rem;
-}
-
-// t2: noisy = latent + U(-Q/2, Q/2) (one draw per latent per step), grad = 0, over the footprint
-__global__ void prep_kernel(const __grid_constant__ PrepParams p) {
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.box_start[p.nbox]) return;
-    int b;
-    int64_t li;
-    box_locate(p.box, p.box_start, p.nbox, i, b, li);
-    float v = p.latents[li];
-    if (p.noise_on) {
-        const uint4 r = philox4x32_10(make_uint4((uint32_t)((uint64_t)li >> 2), (uint32_t)((uint64_t)li >> 34), p.step,
-                                                 0x4E4F4953u),
-                                      make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32)));
-        const uint32_t w = (li & 3) == 0 ? r.x : (li & 3) == 1 ? r.y : (li & 3) == 2 ? r.z : r.w;
-        // u = (2 (w >> 9) + 1) 2^-24 in (0, 1); noise = (u - 1/2) Q, exact in fp32
-        const float u = (float)(2u * (w >> 9) + 1u) * 5.9604644775390625e-8f;
-        v += (u - 0.5f) * (1.0f / (float)(1 << p.box[b].bits));
-    }
-    p.noisy[li] = __float2half_rn(v);
-    p.grad_lat[li] = 0.0f;
 }
 
 // ------------------------------------------------------------------ fused forward + backward
@@ -161,9 +145,10 @@ __device__ __forceinline__ uint32_t h2u(float a, float b) { return pack_half2(a,
 // fp16 SW128 weight image of the current fp32 master weights (t3): W1 (+ b1 at column D, it
 // multiplies X's constant 1), W2, W3 (16 rows); b2 and b3 as fp32 values of their fp16 rounding
 // (R14), added in the epilogues
-__global__ void train_wimg_kernel(const float* __restrict__ w, int D, int c, uint8_t* __restrict__ img) {
+constexpr int WIMG_ITEMS = 3 * 4096 + HID + 16;
+__device__ __forceinline__ void train_wimg_item(int i, const float* __restrict__ w, int D, int c, uint8_t* __restrict__ img) {
     using S = TrainSmem;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= WIMG_ITEMS) return;
     const int P1 = D * HID;
     if (i >= 3 * 4096) {
         const int j = i - 3 * 4096;
@@ -191,6 +176,31 @@ __global__ void train_wimg_kernel(const float* __restrict__ w, int D, int c, uin
     *reinterpret_cast<__half*>(img + base + sw128_offset(r, k)) = __float2half_rn(v);
 }
 
+// t2: noisy = latent + U(-Q/2, Q/2) (one draw per latent per step), grad = 0, over the footprint
+__global__ void prep_kernel(const __grid_constant__ PrepParams p) {
+    if ((int)blockIdx.x >= p.prep_blocks) {
+        if (p.wimg) train_wimg_item(((int)blockIdx.x - p.prep_blocks) * blockDim.x + threadIdx.x, p.params, p.D, p.c, p.wimg);
+        return;
+    }
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.box_start[p.nbox]) return;
+    int b;
+    int64_t li;
+    box_locate(p.box, p.box_start, p.nbox, i, b, li);
+    float v = p.latents[li];
+    if (p.noise_on) {
+        const uint4 r = philox4x32_10(make_uint4((uint32_t)((uint64_t)li >> 2), (uint32_t)((uint64_t)li >> 34), p.step,
+                                                 0x4E4F4953u),
+                                      make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32)));
+        const uint32_t w = (li & 3) == 0 ? r.x : (li & 3) == 1 ? r.y : (li & 3) == 2 ? r.z : r.w;
+        // u = (2 (w >> 9) + 1) 2^-24 in (0, 1); noise = (u - 1/2) Q, exact in fp32
+        const float u = (float)(2u * (w >> 9) + 1u) * 5.9604644775390625e-8f;
+        v += (u - 0.5f) * (1.0f / (float)(1 << p.box[b].bits));
+    }
+    p.noisy[li] = __float2half_rn(v);
+    p.grad_lat[li] = 0.0f;
+}
+
 template <int C0, int C1>
 __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_constant__ TrainParams p) {
     using S = TrainSmem;
@@ -210,7 +220,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     const int wg = warp >> 2, q = warp & 3, row = q * 32 + lane;
     const int c = p.c;
 
-    // ---- weight images (fp16, SW128 K-major, built once per step by train_wimg_kernel); the
+    // ---- weight images (fp16, SW128 K-major, built once per step by the trailing blocks of prep_kernel); the
     // same images serve the backward MMAs through MN-major descriptors (W^T without a copy)
     for (uint32_t i = tid; i < S::WEND / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.wimg) + i);
@@ -727,39 +737,52 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
 }
 
 // fixed-order reduction of the per-CTA partials (deterministic), scaled by 1/(B c): block =
-// 32 parameters x 8 partial groups; group g sums partials g, g+8, ... (four independent
-// accumulators, combined in a fixed order); the 8 group sums are then added in order.
-__global__ void reduce_kernel(const float* __restrict__ partial, size_t part_stride, const float* __restrict__ loss_partial,
-                              int nparts, int P, float inv_bc, float* __restrict__ grad, float* __restrict__ loss,
-                              int32_t* __restrict__ status) {
+// 32 parameters x 8 partial groups; group g owns partials g, g+8, ... and issues all of its
+// (<= RED_MAXK) loads before summing them in order; the 8 group sums are then added in
+// order.  Block 0 also reduces the loss partials with a fixed-shape tree.
+constexpr int RED_MAXK = 32;  // nparts <= 8 * RED_MAXK (grid <= 256 CTAs)
+__global__ void __launch_bounds__(256) reduce_kernel(const float* __restrict__ partial, size_t part_stride,
+                                                     const float* __restrict__ loss_partial, int nparts, int P,
+                                                     float inv_bc, float* __restrict__ grad, float* __restrict__ loss,
+                                                     int32_t* __restrict__ status) {
     __shared__ float s[8][33];
+    __shared__ float sl[256];
     const int px = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int i = blockIdx.x * 32 + px;
-    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-    if (i < P) {
-        int w = g;
-        for (; w + 24 < nparts; w += 32) {
-            a0 += __ldg(partial + (size_t)w * part_stride + i);
-            a1 += __ldg(partial + (size_t)(w + 8) * part_stride + i);
-            a2 += __ldg(partial + (size_t)(w + 16) * part_stride + i);
-            a3 += __ldg(partial + (size_t)(w + 24) * part_stride + i);
-        }
-        for (; w < nparts; w += 8) a0 += __ldg(partial + (size_t)w * part_stride + i);
+    float v[RED_MAXK];
+#pragma unroll
+    for (int k = 0; k < RED_MAXK; ++k) {
+        const int w = g + 8 * k;
+        v[k] = (i < P && w < nparts) ? __ldg(partial + (size_t)w * part_stride + i) : 0.0f;
     }
-    s[g][px] = (a0 + a1) + (a2 + a3);
+    float t = 0.0f;
+#pragma unroll
+    for (int k = 0; k < RED_MAXK; ++k) t += v[k];
+    s[g][px] = t;
+    if (blockIdx.x == 0) {
+        const int nl = nparts * TRAIN_WG;  // <= 2 * 256
+        float l = 0.0f;
+        if ((int)threadIdx.x < nl) l = loss_partial[threadIdx.x];
+        if ((int)threadIdx.x + 256 < nl) l += loss_partial[threadIdx.x + 256];
+        sl[threadIdx.x] = l;
+    }
     __syncthreads();
     if (g == 0 && i < P) {
-        float t = 0.0f;
+        float u = 0.0f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) t += s[k][px];
-        grad[i] = t * inv_bc;
+        for (int k = 0; k < 8; ++k) u += s[k][px];
+        grad[i] = u * inv_bc;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        float t = 0.0f;
-        for (int w = 0; w < nparts * TRAIN_WG; ++w) t += loss_partial[w];
-        const float l = t * inv_bc;
-        *loss = l;
-        if (!isfinite(l) && status) atomicOr(status, (int)NTC_ERR_NONFINITE);
+    if (blockIdx.x == 0) {
+        for (int h = 128; h > 0; h >>= 1) {
+            if ((int)threadIdx.x < h) sl[threadIdx.x] += sl[threadIdx.x + h];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const float l = sl[0] * inv_bc;
+            *loss = l;
+            if (!isfinite(l) && status) atomicOr(status, (int)NTC_ERR_NONFINITE);
+        }
     }
 }
 
@@ -1087,7 +1110,12 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         pp.step = (uint32_t)hp->step;
         pp.noise_on = hp->noise_on;
         if (hp->dense_latent_adam) cudaMemsetAsync(buf->grad_lat, 0, sizeof(float) * NL, st);
-        prep_kernel<<<(n + 255) / 256, 256, 0, st>>>(pp);
+        pp.prep_blocks = (n + 255) / 256;
+        pp.params = buf->params;
+        pp.D = 4 * d->c0 + d->c1 + 13;
+        pp.c = d->channels;
+        pp.wimg = t->wimg;
+        prep_kernel<<<pp.prep_blocks + (WIMG_ITEMS + 255) / 256, 256, 0, st>>>(pp);
         // t1, t3-t7
         TrainParams tp;
         memset(&tp, 0, sizeof tp);
@@ -1137,14 +1165,13 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.noisy = reinterpret_cast<const __half*>(buf->noisy);
         tp.grad_lat = buf->grad_lat;
         tp.wimg = t->wimg;
-        train_wimg_kernel<<<(3 * 4096 + 80 + 255) / 256, 256, 0, st>>>(buf->params, 4 * d->c0 + d->c1 + 13, d->channels,
-                                                                 t->wimg);
         tp.partial = t->partial;
         tp.loss_partial = t->loss_partial;
         tp.P = (int32_t)P;
         if (const char* dbg = getenv("NTC_DEBUG_TRAIN")) tp.debug_flags = atoi(dbg);
         tp.freeze = hp->freeze_latents;
-        const int grid = (int)std::min<int64_t>(t->num_sms, (tiles + TRAIN_WG - 1) / TRAIN_WG);
+        const int grid = (int)std::min<int64_t>(std::min<int64_t>(t->num_sms, 8 * RED_MAXK),
+                                                (tiles + TRAIN_WG - 1) / TRAIN_WG);
         auto* k = train_kernel<8, 12>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TrainSmem::BYTES);
         if (e == cudaSuccess) {
