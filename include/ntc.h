@@ -53,11 +53,13 @@ typedef struct {
     int32_t activation;
 } ntc_desc;
 
-/* One random-access query (8 bytes): texel (x, y) of mip `mip`. */
+/* One random-access query (8 bytes): texel (x, y) of mip `mip`; `material` indexes the
+ * material array of ntc_decode_texels_multi (ignored by the single-material calls). */
 typedef struct {
     uint16_t x, y;
     uint8_t mip;
-    uint8_t pad[3];
+    uint8_t material;
+    uint8_t pad[2];
 } ntc_query;
 
 const char* ntc_last_error(void);
@@ -122,6 +124,24 @@ ntc_status ntc_decode_chain(const ntc_material* m, uint16_t* out, ntc_stream str
  * into the same chain layout as ntc_decode_chain (other texels of out are not written).  */
 ntc_status ntc_decode_chain_part(const ntc_material* m, int32_t part, int32_t nparts, uint16_t* out,
                                  ntc_stream stream);
+
+/* Multi-material random-access decode (the B200 analog of the paper's
+ * divergence handling for neighbouring pixels of different materials):
+ * queries of up to NTC_MAX_MATERIALS materials in one call.  The library buckets the queries
+ * by q[i].material on the device (count, scan, scatter into scratch), then one persistent
+ * launch walks the material-sorted tile list; every 128-texel tile has a single weight set,
+ * which a CTA swaps in SMEM only when its share of the list crosses a material boundary.
+ * mats: host array [n_mats] of materials that all share one ntc_desc (same dimensions,
+ * profile, channels and depth; else NTC_ERR_INVALID_ARGUMENT).  q: device [n] queries;
+ * out: device fp16 [n][c], row i for query i (input order).  A query whose material index is
+ * >= n_mats, or whose texel is out of range, gets a NaN row and sets NTC_ERR_OUT_OF_RANGE in
+ * *status (device int32, may be NULL).  scratch: device, >= ntc_decode_multi_scratch_bytes(n)
+ * bytes, 16-byte aligned, owned by the caller.  n <= 2^31 - 1.                           */
+#define NTC_MAX_MATERIALS 256
+int64_t ntc_decode_multi_scratch_bytes(int64_t n);
+ntc_status ntc_decode_texels_multi(const ntc_material* const* mats, int32_t n_mats, const ntc_query* q, int64_t n,
+                                   uint16_t* out, int32_t* status, void* scratch, int64_t scratch_bytes,
+                                   ntc_stream stream);
 
 /* Texture filtering on top of random-access decode.
  * uvl: device fp32 [n][3] = (u, v, lod): u, v in [0,1) (texel x of mip m has centre

@@ -77,6 +77,10 @@ ABI_FUNCTIONS = {
     "ntc_decode_chain": (ctypes.c_int, [ctypes.c_void_p] * 3),
     "ntc_decode_chain_part": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
                                              ctypes.c_void_p]),
+    "ntc_decode_multi_scratch_bytes": (ctypes.c_int64, [ctypes.c_int64]),
+    "ntc_decode_texels_multi": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                               ctypes.c_void_p]),
     "ntc_footprint_size": (ctypes.c_int64, [ctypes.c_void_p] * 2),
     "ntc_filter_scratch_bytes": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),
     "ntc_filter_texels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
@@ -216,10 +220,14 @@ class Material:
             pass
 
 
-def pack_queries(xym: torch.Tensor) -> torch.Tensor:
-    """(n, 3) int tensor (x, y, mip) -> int64 [n] holding ntc_query structs (8 bytes)."""
+def pack_queries(xym: torch.Tensor, material: torch.Tensor = None) -> torch.Tensor:
+    """(n, 3) int tensor (x, y, mip) [+ material index per query] -> int64 [n] holding
+    ntc_query structs (8 bytes)."""
     x, y, m = xym[:, 0].long(), xym[:, 1].long(), xym[:, 2].long()
-    return (x & 0xFFFF) | ((y & 0xFFFF) << 16) | ((m & 0xFF) << 32)
+    q = (x & 0xFFFF) | ((y & 0xFFFF) << 16) | ((m & 0xFF) << 32)
+    if material is not None:
+        q = q | ((material.long().to(q.device) & 0xFF) << 40)
+    return q
 
 
 def ntc_decode_texels(mat: Material, queries: torch.Tensor, out: torch.Tensor, status: torch.Tensor = None,
@@ -227,6 +235,24 @@ def ntc_decode_texels(mat: Material, queries: torch.Tensor, out: torch.Tensor, s
     assert queries.dtype == torch.int64 and out.dtype == torch.float16
     _check(lib().ntc_decode_texels(mat.handle, _ptr(queries), queries.numel(), _ptr(out), _ptr(status),
                                    _stream(stream)))
+
+
+def ntc_decode_multi_scratch_bytes(n: int) -> int:
+    return int(lib().ntc_decode_multi_scratch_bytes(n))
+
+
+def ntc_decode_texels_multi(mats, queries: torch.Tensor, out: torch.Tensor, status: torch.Tensor = None,
+                            scratch: torch.Tensor = None, stream=None):
+    """Queries of several materials (index in bits 40-47, see pack_queries) in one call."""
+    assert queries.dtype == torch.int64 and out.dtype == torch.float16
+    n = queries.numel()
+    need = ntc_decode_multi_scratch_bytes(n)
+    if scratch is None:
+        scratch = torch.empty(need, dtype=torch.uint8, device=queries.device)
+    arr = (ctypes.c_void_p * len(mats))(*[m.handle.value for m in mats])
+    _check(lib().ntc_decode_texels_multi(arr, len(mats), _ptr(queries), n, _ptr(out), _ptr(status), _ptr(scratch),
+                                         scratch.numel() * scratch.element_size(), _stream(stream)))
+    return scratch
 
 
 def ntc_decode_mip(mat: Material, mip: int, out: torch.Tensor, row_stride_elems: int = None, stream=None):

@@ -111,8 +111,8 @@ struct Fetch {
 // fractional offsets are multiples of 1/16 (r1 / w_m >= 1/8 for every compiled profile),
 // so the bilinear weights are exact multiples of 1/256.
 template <class P>
-__device__ __forceinline__ void fetch_texel(const DecodeParams& p, int m, int x, int y, Fetch<P>& f,
-                                            int32_t* dbg_addr) {
+__device__ __forceinline__ void fetch_texel(const DecodeParams& p, const uint8_t* grids, int m, int x, int y,
+                                            Fetch<P>& f, int32_t* dbg_addr) {
     f.m = m;
     f.x = x;
     f.y = y;
@@ -144,8 +144,8 @@ __device__ __forceinline__ void fetch_texel(const DecodeParams& p, int m, int x,
         ty1[0] = max(k, 0);
         ty1[1] = min(k + 1, g.r1 - 1);
     }
-    const uint8_t* g0 = p.grids + g.off0;
-    const uint8_t* g1 = p.grids + g.off1;
+    const uint8_t* g0 = grids + g.off0;
+    const uint8_t* g1 = grids + g.off1;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         f.g0[t] = load_cell<P::CELL0>(g0, (uint32_t)(ty0[t >> 1] * g.r0 + tx0[t & 1]));

@@ -65,4 +65,19 @@ struct DecodeParams {
     float b3[16];                  // output bias, added in the output epilogue
 };
 
+// Multi-material decode: per-material device records in the parameter
+// space; the bucketing of the queries by material lives in device scratch (multi.cu).
+struct MatRec {
+    const uint8_t* grids;
+    const uint4* wimg;
+    float b3[16];
+};
+struct MultiTable {
+    int32_t n_mats;
+    const int32_t* seg;     // [n_mats + 1] offsets of each material's queries in perm
+    const int32_t* tstart;  // [n_mats + 1] first tile of each material; [n_mats] = total tiles
+    const int32_t* perm;    // query indices grouped by material
+    MatRec rec[NTC_MAX_MATERIALS];
+};
+
 }  // namespace ntc

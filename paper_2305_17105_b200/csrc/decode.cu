@@ -72,12 +72,20 @@ struct DecodeSmem {
     static constexpr uint32_t BYTES = 1024 + WIMG + ONES + NWG * 2 * ABUF + 128 /*pe*/ + 128 /*bars*/ + 16;
 };
 
+// The tile range a CTA is working through, with the material it belongs to (uniform).
+struct Run {
+    const uint8_t* grids;
+    const float* b3;
+    int ts0, seg0, cnt;  // multi: first tile, first perm slot and query count of the material
+    const int32_t* perm;
+};
+
 // resolve the texel of row `row` of `tile`, its output address, and issue its latent loads
-template <class P>
-__device__ __forceinline__ void fetch_tile(const DecodeParams& p, int tile, int row, Fetch<P>& f) {
+template <class P, bool MULTI>
+__device__ __forceinline__ void fetch_tile(const DecodeParams& p, const Run R, int tile, int row, Fetch<P>& f) {
     int m = 0, x = 0, y = 0;
     bool valid, bad = false;
-    if (p.mode == 0) {
+    if (!MULTI && p.mode == 0) {
         int mi = 0;
         while (tile >= p.tile_start[mi + 1]) ++mi;
         m = p.mip_first + mi;
@@ -90,8 +98,15 @@ __device__ __forceinline__ void fetch_tile(const DecodeParams& p, int tile, int 
         }
         f.dst = p.out + (p.out_off[mi] + (int64_t)y * p.row_stride[mi] + x * p.c);
     } else {
-        const int64_t qi = (int64_t)tile * TILE_M + row;
-        valid = qi < p.nq;
+        int64_t qi;
+        if (MULTI) {
+            const int local = (tile - R.ts0) * TILE_M + row;
+            valid = local < R.cnt;
+            qi = valid ? (int64_t)__ldg(R.perm + R.seg0 + local) : 0;
+        } else {
+            qi = (int64_t)tile * TILE_M + row;
+            valid = qi < p.nq;
+        }
         if (valid) {
             const uint2 qq = __ldg(reinterpret_cast<const uint2*>(p.q) + qi);
             x = (int)(qq.x & 0xFFFFu);
@@ -107,7 +122,7 @@ __device__ __forceinline__ void fetch_tile(const DecodeParams& p, int tile, int 
     }
     f.valid = valid;
     f.bad = bad;
-    fetch_texel<P>(p, m, x, y, f, nullptr);
+    fetch_texel<P>(p, MULTI ? R.grids : p.grids, m, x, y, f, nullptr);
 }
 
 // a7 store of one texel's c fp16 channels (o = 8 packed pairs).  c is uniform, so the
@@ -151,8 +166,8 @@ struct Ctx {
     uint64_t adesc;     // SW128 K-major descriptor of abuf
 };
 
-template <class P, int HM>
-__global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
+template <class P, int HM, bool MULTI>
+__device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTable* mt) {
     using S = DecodeSmem<P, HM>;
     constexpr int NW = S::NWG;
     extern __shared__ uint8_t smem_raw[];
@@ -167,7 +182,8 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wg = warp >> 2, q = warp & 3, row = q * 32 + lane;
 
-    for (uint32_t i = tid; i < S::WIMG / 16; i += blockDim.x) reinterpret_cast<uint4*>(s_w)[i] = p.wimg[i];
+    if (!MULTI)
+        for (uint32_t i = tid; i < S::WIMG / 16; i += blockDim.x) reinterpret_cast<uint4*>(s_w)[i] = p.wimg[i];
     for (uint32_t i = tid; i < S::ONES / 16; i += blockDim.x) {
         const uint32_t r = i >> 3, chunk = i & 7;  // 16-byte chunk `chunk` of row r
         const bool one = chunk == (r & 7);          // logical chunk 0 lands at physical r&7
@@ -205,13 +221,18 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
             named_bar_arrive(1 + wg * 2 + C.id, 128);
     };
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
-    const int ntiles = p.mode == 0 ? p.n_tiles : (int)((p.nq + TILE_M - 1) / TILE_M);
-    const int stride = (int)gridDim.x * NW * 2;  // tiles advance by 2 contexts per warpgroup
+    // single material: tiles blockIdx-strided over [first, ntiles); multi: per-run ranges
+    int ntiles = p.mode == 0 ? p.n_tiles : (int)((p.nq + TILE_M - 1) / TILE_M);
+    int stride = (int)gridDim.x * NW * 2;  // tiles advance by 2 contexts per warpgroup
+    Run R;
+    R.grids = nullptr;
+    R.b3 = nullptr;
+    R.perm = MULTI ? mt->perm : nullptr;
+    R.ts0 = R.seg0 = R.cnt = 0;
 
     Ctx<P> cx[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-        cx[c].tile = (p.mode == 0 ? p.tile_first : 0) + ((int)blockIdx.x * NW + wg) * 2 + c;
         cx[c].phase = 0;
         cx[c].abuf = smem_u32(s_a + (wg * 2 + c) * S::ABUF);
         cx[c].tcol = tmem + (uint32_t)(wg * 128 + c * 64);
@@ -219,7 +240,10 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
         cx[c].id = c;
         cx[c].iq = (wg * 2 + c) & 3;
         cx[c].adesc = umma_desc_k_sw128(cx[c].abuf);
-        if (cx[c].tile < ntiles) fetch_tile<P>(p, cx[c].tile, row, cx[c].nxt);
+        if (!MULTI) {
+            cx[c].tile = (p.mode == 0 ? p.tile_first : 0) + ((int)blockIdx.x * NW + wg) * 2 + c;
+            if (cx[c].tile < ntiles) fetch_tile<P, MULTI>(p, R, cx[c].tile, row, cx[c].nxt);
+        }
     }
 
     // P0: assemble X of the context's tile from its prefetched latents, MMA1, prefetch next
@@ -245,7 +269,7 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
             mma_commit(C.bar);
         }
         const int nt = C.tile + stride;
-        if (nt < ntiles) fetch_tile<P>(p, nt, row, C.nxt);  // loads overlap the MLP
+        if (nt < ntiles) fetch_tile<P, MULTI>(p, R, nt, row, C.nxt);  // loads overlap the MLP
     };
     // P1..P(HM+1): wait for the previous MMA, epilogue to the A tile, next layer's MMA
     auto phase_hidden = [&](Ctx<P>& C, int layer) {
@@ -282,29 +306,79 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
         uint32_t o[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            o[k] = pack_half2(__saturatef(__uint_as_float(r[2 * k]) + p.b3[2 * k]),
-                              __saturatef(__uint_as_float(r[2 * k + 1]) + p.b3[2 * k + 1]));
+            o[k] = pack_half2(__saturatef(__uint_as_float(r[2 * k]) + (MULTI ? R.b3 : p.b3)[2 * k]),
+                              __saturatef(__uint_as_float(r[2 * k + 1]) + (MULTI ? R.b3 : p.b3)[2 * k + 1]));
         store_output(p, C.dst, C.valid, C.bad, o);  // R13: clamp [0,1]
         tc_fence_before();
         C.tile += stride;
         phase0(C);
     };
 
-    phase0(cx[0]);
-    phase0(cx[1]);
-    while (cx[0].tile < ntiles || cx[1].tile < ntiles) {
+    // tiles first + 2 wg + c, advancing by `stride`, up to `ntiles` (exclusive), through the
+    // two-context pipeline; returns with every context drained (all MMAs waited for)
+    auto run = [&](int first) {
+        if (MULTI) {
 #pragma unroll
-        for (int layer = 0; layer <= HM; ++layer) {
-            phase_hidden(cx[0], layer);
-            phase_hidden(cx[1], layer);
+            for (int c = 0; c < 2; ++c) {
+                cx[c].tile = first + wg * 2 + c;
+                if (cx[c].tile < ntiles) fetch_tile<P, MULTI>(p, R, cx[c].tile, row, cx[c].nxt);
+            }
         }
-        phase_out(cx[0]);
-        phase_out(cx[1]);
+        phase0(cx[0]);
+        phase0(cx[1]);
+        while (cx[0].tile < ntiles || cx[1].tile < ntiles) {
+#pragma unroll
+            for (int layer = 0; layer <= HM; ++layer) {
+                phase_hidden(cx[0], layer);
+                phase_hidden(cx[1], layer);
+            }
+            phase_out(cx[0]);
+            phase_out(cx[1]);
+        }
+    };
+    if constexpr (!MULTI) {
+        run(0);  // tiles and their first fetches were set up with the contexts
+    } else {
+        // a contiguous share of the material-sorted tile list; one weight image at a time
+        const int T = __ldg(mt->tstart + mt->n_mats);
+        const int c0 = (int)((int64_t)T * blockIdx.x / gridDim.x), c1 = (int)((int64_t)T * (blockIdx.x + 1) / gridDim.x);
+        int m = 0;
+        while (m < mt->n_mats && __ldg(mt->tstart + m + 1) <= c0) ++m;
+        for (int pos = c0; pos < c1 && m < mt->n_mats; ++m) {
+            const int ts1 = __ldg(mt->tstart + m + 1), e = min(c1, ts1);
+            if (e <= pos) continue;
+            // the previous run is drained: its MMAs no longer read the weight image
+            __syncthreads();
+            const uint4* wsrc = mt->rec[m].wimg;
+            for (uint32_t i = tid; i < S::WIMG / 16; i += blockDim.x) reinterpret_cast<uint4*>(s_w)[i] = __ldg(wsrc + i);
+            fence_proxy_async_smem();
+            __syncthreads();
+            R.grids = mt->rec[m].grids;
+            R.b3 = mt->rec[m].b3;
+            R.ts0 = __ldg(mt->tstart + m);
+            R.seg0 = __ldg(mt->seg + m);
+            R.cnt = __ldg(mt->seg + m + 1) - R.seg0;
+            ntiles = e;
+            stride = NW * 2;
+            run(pos);
+            pos = e;
+        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <class P, int HM>
+__global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
+    decode_body<P, HM, false>(p, nullptr);
+}
+
+template <class P, int HM>
+__global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1)
+    decode_multi_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ MultiTable mt) {
+    decode_body<P, HM, true>(p, &mt);
 }
 
 // Tests only: the same addressing + assembly, written to global memory in canonical order.
@@ -322,7 +396,7 @@ __global__ void debug_assemble_kernel(const __grid_constant__ DecodeParams p) {
         x = y = 0;
     }
     Fetch<P> f;
-    fetch_texel<P>(p, m, x, y, f, p.dbg_addr + i * 17);
+    fetch_texel<P>(p, p.grids, m, x, y, f, p.dbg_addr + i * 17);
     uint32_t w[P::K1W];
     assemble_words<P>(p, s_pe, f, w);
     uint16_t* X = p.dbg_X + i * P::D;
@@ -411,6 +485,20 @@ cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cuda
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
         if (e != cudaSuccess) return e;
         k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p);
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t launch_decode_multi(int pid, int hm, const DecodeParams& p, const MultiTable& mt, int grid,
+                                cudaStream_t s) {
+    return dispatch(pid, hm, [&](auto pr, auto h) {
+        using PP = decltype(pr);
+        constexpr int HMv = decltype(h)::value;
+        using SS = DecodeSmem<PP, HMv>;
+        auto* k = decode_multi_kernel<PP, HMv>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
+        if (e != cudaSuccess) return e;
+        k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p, mt);
         return cudaGetLastError();
     });
 }
