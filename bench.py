@@ -9,6 +9,8 @@ One step = one pass of the hot path over synthetic inputs resident in HBM:
   train   : ntc_train_step(GRADS|APPLY) on 4 random 256^2 crops at LOD 0 (262,144 texels)
             of a 4096^2 9-channel material (configs[3]), when the library provides it.
 L2 is flushed (256 MiB write) before every timed step, outside the CUDA-event window.
+Extra lines at N=1 (--no-extras skips them): `random` = configs[2]'s 2^24 random-access
+queries on a 4096^2 16-channel material; `multi` = the Table 4 screen workload over 8 materials (f3).
 Multi-GPU (torchrun): weak scaling, one independent material per rank (configs[4]:
 decode needs no collective); time = max over ranks of the device time.
 """
@@ -241,9 +243,93 @@ def run_ours(args, rank, world, local_rank):
                                      "unit": "TFLOP/s", "frac": round(tflops / peak_tf, 4)}}
     # e2e through the public API from pinned host buffers (rank 0 and every rank alike)
     res["e2e"] = e2e(args, ntc, torch, d, codes, wts, dev, world)
+    if world == 1 and not args.no_extras:
+        res["random"] = bench_random(args, ntc, torch, dev, flush)
+        res["multi"] = bench_multi(args, ntc, torch, dev, flush)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(d, codes, wts, budget_s=args.cpu_budget)
     return res
+
+
+def _device_time(torch, fn, flush, reps):
+    """mean device seconds of fn() over `reps` runs, L2 flushed before each (outside the events)"""
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    tot = 0.0
+    for _ in range(reps):
+        flush.zero_()
+        e0.record(s)
+        fn()
+        e1.record(s)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1) / 1e3
+    return tot / reps
+
+
+def bench_random(args, ntc, torch, dev, flush):
+    """configs[2] (C3b): 2^24 random-access queries, area-uniform over the chain, random order,
+    on a 4096^2 16-channel NTC 0.2 material (ntc_decode_texels)."""
+    d = Profile.named("ntc0.2", W, 16)
+    seed = SEED_BASE + 2
+    mat = ntc.Material(d, torch.from_numpy(gen_codes(seed, ntc.grid_list(d))).to(dev),
+                       torch.from_numpy(gen_weights_f16(seed + 1, d.input_dim, 16).view(np.int16)).to(dev))
+    n = 1 << 24
+    q = ntc.pack_queries(torch.from_numpy(gen_queries(seed + 2, W, n, "area")).to(dev))
+    out = torch.empty((n, 16), dtype=torch.float16, device=dev)
+    t = _device_time(torch, lambda: ntc.ntc_decode_texels(mat, q, out), flush, max(3, min(args.steps, 10)))
+    pk, _ = _peaks()
+    tf = decode_flops_per_texel(d) * n / t / 1e12
+    return {"metric": "random-access decoded Gtexel/s", "value": n / t / 1e9, "unit": UNIT,
+            "workload": "4096^2 x 16ch NTC0.2, 2^24 area-uniform random queries (configs[2])",
+            "ms_per_step": t * 1e3, "roofline": {"bound": "tensor", "achieved": round(tf, 2),
+                                                 "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                                                 "frac": round(tf / pk["bf16_tflops"], 4)}}
+
+
+def screen_queries(n_mats, block=64, sw=3840, sh=2160, seed=SEED_BASE + 40):
+    """Table 4 analog: a full-screen quad at 3840x2160 sampling mip 0 of a 4096^2
+    texture, queries in screen (row-major) order; every 64x64 screen block shows one of
+    `n_mats` materials (seeded), so material runs are long but interleaved across the frame."""
+    py, px = np.meshgrid(np.arange(sh), np.arange(sw), indexing="ij")
+    x = ((px.astype(np.int64) * 2 + 1) * W) // (2 * sw)
+    y = ((py.astype(np.int64) * 2 + 1) * W) // (2 * sh)
+    xym = np.stack([x.ravel(), y.ravel(), np.zeros(x.size, np.int64)], 1).astype(np.int32)
+    tab = np.random.default_rng(seed).integers(0, n_mats, ((sh + block - 1) // block, (sw + block - 1) // block))
+    mid = tab[py // block, px // block].ravel().astype(np.int32)
+    return xym, mid
+
+
+def bench_multi(args, ntc, torch, dev, flush, n_mats=8):
+    """f3: the Table 4 screen workload (8,294,400 mip-0 queries in screen order) over 8 materials
+    (4096^2, 8 channels, NTC 0.2), one ntc_decode_texels_multi call (device bucketing + one
+    persistent decode launch); also the worst case (material uniformly random per query) and
+    the same screen queries on a single material through ntc_decode_texels."""
+    d = Profile.named("ntc0.2", W, 8)
+    mats = []
+    for k in range(n_mats):
+        seed = SEED_BASE + 4 + k  # configs[4]: per-material seed = base + material id
+        mats.append(ntc.Material(d, torch.from_numpy(gen_codes(seed, ntc.grid_list(d))).to(dev),
+                                 torch.from_numpy(gen_weights_f16(seed + 1, d.input_dim, 8).view(np.int16)).to(dev)))
+    xym, mid = screen_queries(n_mats)
+    n = xym.shape[0]
+    reps = max(3, min(args.steps, 10))
+    xym_d = torch.from_numpy(xym).to(dev)
+    q = ntc.pack_queries(xym_d, torch.from_numpy(mid).to(dev))
+    qr = ntc.pack_queries(xym_d, torch.from_numpy(
+        np.random.default_rng(SEED_BASE + 41).integers(0, n_mats, n).astype(np.int32)).to(dev))
+    q1 = ntc.pack_queries(xym_d)
+    out = torch.empty((n, 8), dtype=torch.float16, device=dev)
+    scratch = torch.empty(ntc.ntc_decode_multi_scratch_bytes(n), dtype=torch.uint8, device=dev)
+    t = _device_time(torch, lambda: ntc.ntc_decode_texels_multi(mats, q, out, scratch=scratch), flush, reps)
+    tr = _device_time(torch, lambda: ntc.ntc_decode_texels_multi(mats, qr, out, scratch=scratch), flush, reps)
+    t1 = _device_time(torch, lambda: ntc.ntc_decode_texels(mats[0], q1, out), flush, reps)
+    return {"metric": "multi-material decoded Gtexel/s", "value": n / t / 1e9, "unit": UNIT,
+            "workload": f"Table 4 analog: 3840x2160 screen-order mip-0 queries ({n}), {n_mats} x 4096^2 x 8ch "
+                        "NTC0.2 materials, one material per 64x64 screen block",
+            "ms_per_step": t * 1e3, "gpu_launches_per_step": 5,
+            "random_material_per_query": {"value": n / tr / 1e9, "ms_per_step": tr * 1e3},
+            "single_material_same_queries": {"value": n / t1 / 1e9, "ms_per_step": t1 * 1e3}}
 
 
 def e2e(args, ntc, torch, d, codes, wts, dev, world):
@@ -342,6 +428,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip the random-access and multi-material lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
