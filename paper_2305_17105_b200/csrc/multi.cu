@@ -33,19 +33,44 @@ namespace {
 constexpr int64_t OFF_COUNT = 0, OFF_SEG = 1024, OFF_TSTART = 2112, OFF_CURSOR = 3200, OFF_PERM = 4352;
 constexpr int MULTI_ITEMS = 8;  // queries per thread in the scatter pass
 
+// SMEM counter add with a warp fast path: when every active lane has the same key (long runs
+// in screen-ordered query streams) one atomic serves the warp; otherwise one atomic per lane.
+// Returns this lane's slot (old value + rank among the lanes sharing the key).
+__device__ __forceinline__ int agg_add(int32_t* h, int key, bool active) {
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, active);
+    if (act == 0) return 0;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(act) - 1;
+    const int k0 = __shfl_sync(0xFFFFFFFFu, key, leader);
+    if (__all_sync(0xFFFFFFFFu, !active || key == k0)) {
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&h[k0], __popc(act));
+        base = __shfl_sync(0xFFFFFFFFu, base, leader);
+        return base + __popc(act & ((1u << lane) - 1u));
+    }
+    return active ? atomicAdd(&h[key], 1) : 0;
+}
+
 __global__ void multi_count_kernel(const ntc_query* __restrict__ q, int64_t n, int n_mats, int c,
                                    int32_t* __restrict__ count, uint16_t* __restrict__ out,
                                    int32_t* __restrict__ status) {
     __shared__ int32_t h[NTC_MAX_MATERIALS];
     for (int i = threadIdx.x; i < NTC_MAX_MATERIALS; i += blockDim.x) h[i] = 0;
     __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * MULTI_ITEMS;
+    int mat[MULTI_ITEMS];
+#pragma unroll
+    for (int k = 0; k < MULTI_ITEMS; ++k) {  // all loads in flight first
+        const int64_t i = base + (int64_t)k * blockDim.x + threadIdx.x;
+        mat[k] = i < n ? (int)((__ldg(reinterpret_cast<const uint2*>(q) + i).y >> 8) & 0xFFu) : -1;
+    }
     bool badseen = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int m = (int)((__ldg(reinterpret_cast<const uint2*>(q) + i).y >> 8) & 0xFFu);
-        if (m < n_mats) {
-            atomicAdd(&h[m], 1);
-        } else {
-            for (int k = 0; k < c; ++k) out[i * c + k] = 0x7E00u;  // NaN row
+#pragma unroll
+    for (int k = 0; k < MULTI_ITEMS; ++k) {
+        const int64_t i = base + (int64_t)k * blockDim.x + threadIdx.x;
+        agg_add(h, mat[k] >= 0 && mat[k] < n_mats ? mat[k] : 0, mat[k] >= 0 && mat[k] < n_mats);
+        if (mat[k] >= n_mats) {
+            for (int j = 0; j < c; ++j) out[i * c + j] = 0x7E00u;  // NaN row
             badseen = true;
         }
     }
@@ -92,14 +117,10 @@ __global__ void multi_scatter_kernel(const ntc_query* __restrict__ q, int64_t n,
 #pragma unroll
     for (int k = 0; k < MULTI_ITEMS; ++k) {
         const int64_t i = base + (int64_t)k * blockDim.x + threadIdx.x;
-        mat[k] = -1;
-        if (i < n) {
-            const int m = (int)((__ldg(reinterpret_cast<const uint2*>(q) + i).y >> 8) & 0xFFu);
-            if (m < n_mats) {
-                mat[k] = m;
-                rank[k] = atomicAdd(&h[m], 1);
-            }
-        }
+        const int m = i < n ? (int)((__ldg(reinterpret_cast<const uint2*>(q) + i).y >> 8) & 0xFFu) : n_mats;
+        const bool ok = m < n_mats;
+        mat[k] = ok ? m : -1;
+        rank[k] = agg_add(h, ok ? m : 0, ok);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n_mats; i += blockDim.x)
@@ -141,10 +162,10 @@ extern "C" ntc_status ntc_decode_texels_multi(const ntc_material* const* mats, i
     const ntc_material* m0 = mats[0];
     cudaError_t e = cudaMemsetAsync(count, 0, 4 * NTC_MAX_MATERIALS, st);
     if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
-    const int64_t cblocks = std::min<int64_t>((n + 255) / 256, 4 * (int64_t)m0->num_sms);
-    multi_count_kernel<<<(int)cblocks, 256, 0, st>>>(q, n, n_mats, m0->d.channels, count, out, status);
-    multi_scan_kernel<<<1, NTC_MAX_MATERIALS, 0, st>>>(count, n_mats, seg, tstart, cursor);
     const int64_t per = 256 * MULTI_ITEMS;
+    multi_count_kernel<<<(int)((n + per - 1) / per), 256, 0, st>>>(q, n, n_mats, m0->d.channels, count, out,
+                                                                    status);
+    multi_scan_kernel<<<1, NTC_MAX_MATERIALS, 0, st>>>(count, n_mats, seg, tstart, cursor);
     multi_scatter_kernel<<<(int)((n + per - 1) / per), 256, 0, st>>>(q, n, n_mats, cursor, perm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
