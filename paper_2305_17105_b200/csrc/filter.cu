@@ -34,7 +34,8 @@ __device__ __forceinline__ ntc_query make_q(int x, int y, int m) {
     q.x = (uint16_t)x;
     q.y = (uint16_t)y;
     q.mip = (uint8_t)m;
-    q.pad[0] = q.pad[1] = q.pad[2] = 0;
+    q.material = 0;
+    q.pad[0] = q.pad[1] = 0;
     return q;
 }
 
