@@ -129,7 +129,8 @@ __device__ __forceinline__ uint4 lds_row_chunk(uint32_t tile, int row, int chunk
 }
 
 __device__ __forceinline__ float hgelu(float z) { return z * __saturatef(fmaf(z, 1.0f / 3.0f, 0.5f)); }
-// R15: derivative of the piecewise hardGELU, the middle piece at +-3/2
+// R15: derivative of the piecewise hardGELU, the middle piece at +-3/2 (decided in fp32: the
+// derivative jumps at +-3/2, so the branch must follow the fp32 pre-activation exactly)
 __device__ __forceinline__ float hgelu_d(float z) {
     const float t = fmaf(z, 2.0f / 3.0f, 0.5f);
     return z > 1.5f ? 1.0f : (z < -1.5f ? 0.0f : t);
@@ -510,11 +511,12 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
                     const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
                     uint32_t o[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
+                    for (int e = 0; e < 4; ++e) {  // delta = fp16(dA) * g' in packed fp16
                         const __half2 g2 = *reinterpret_cast<const __half2*>(&gw[e]);
-                        const float2 gf = __half22float2(g2);
                         const int col = 8 * cc + 2 * e;
-                        o[e] = h2u(__uint_as_float(r[col]) * gf.x, __uint_as_float(r[col + 1]) * gf.y);
+                        const uint32_t aw = h2u(__uint_as_float(r[col]), __uint_as_float(r[col + 1]));
+                        const __half2 dv = __hmul2(*reinterpret_cast<const __half2*>(&aw), g2);
+                        o[e] = *reinterpret_cast<const uint32_t*>(&dv);
                     }
                     sts_row_chunk(tG, row, 4 * half + cc, o[0], o[1], o[2], o[3]);
                 }
