@@ -42,7 +42,8 @@ typedef enum {
  * feature-grid profile (Table 2: G^0_0 = W/g0_ratio, C_k x B_k) and the
  * decoder MLP [D, 64, 64, c] (hidden_mats = 1) or [D, 64, 64, 64, c]
  * (hidden_mats = 2, reading R11), D = 4C0 + C1 + 12 + 1, hardGELU
- * (activation = 0).  Compiled profiles: NTC 0.2/0.5/1.0/2.25.     */
+ * (activation = 0) or exact GELU x Phi(x) (activation = 1, PAPER.md:496;
+ * decode: every profile/depth; training: NTC 0.2).  Compiled profiles: NTC 0.2/0.5/1.0/2.25. */
 typedef struct {
     int32_t width;
     int32_t channels;

@@ -77,6 +77,8 @@ def lib():
             "ntco_assemble": (None, [P(Desc), vp, i32, i32, i32, vp]),
             "ntco_hardgelu": (f64, [f64]),
             "ntco_hardgelu_grad": (f64, [f64]),
+            "ntco_gelu": (f64, [f64]),
+            "ntco_gelu_grad": (f64, [f64]),
             "ntco_mlp_forward": (None, [P(Desc), vp, vp, vp]),
             "ntco_decode_texels": (None, [P(Desc), vp, vp, vp, i64, vp, i32]),
             "ntco_decode_mip": (None, [P(Desc), vp, vp, i32, vp, i32]),
@@ -212,6 +214,14 @@ def hardgelu(x):
 
 def hardgelu_grad(x):
     return lib().ntco_hardgelu_grad(float(x))
+
+
+def gelu(x):
+    return lib().ntco_gelu(float(x))
+
+
+def gelu_grad(x):
+    return lib().ntco_gelu_grad(float(x))
 
 
 def mlp_forward(d, params: np.ndarray, X: np.ndarray) -> np.ndarray:

@@ -266,15 +266,31 @@ double ntco_hardgelu_grad(double x) {
     return (2.0 * x + 1.5) / 3.0;
 }
 
+/* Exact GELU (Hendrycks & Gimpel): x Phi(x) = x/2 (1 + erf(x/sqrt 2));
+ * the `activation = 1` variant.                                  */
+double ntco_gelu(double x) { return 0.5 * x * (1.0 + erf(x / sqrt(2.0))); }
+
+/* d/dx x Phi(x) = Phi(x) + x phi(x). */
+double ntco_gelu_grad(double x) {
+    const double Phi = 0.5 * (1.0 + erf(x / sqrt(2.0)));
+    const double phi = exp(-0.5 * x * x) / sqrt(2.0 * 3.14159265358979323846);
+    return Phi + x * phi;
+}
+
+static double act(int32_t a, double x) { return a == 1 ? ntco_gelu(x) : ntco_hardgelu(x); }
+static double act_grad(int32_t a, double x) { return a == 1 ? ntco_gelu_grad(x) : ntco_hardgelu_grad(x); }
+
 typedef struct {
     const double *W[4], *b[4];  /* layers: D->64, (64->64) x hidden_mats, 64->c */
     int32_t nin[4], nout[4], nl;
+    int32_t act;                /* 0 hardGELU, 1 GELU */
 } mlp_view;
 
 static mlp_view mlp_layout(const ntco_desc* d, const double* params) {
     mlp_view v;
     int32_t D = ntco_input_dim(d);
     v.nl = 2 + d->hidden_mats;
+    v.act = d->activation;
     const double* p = params;
     for (int32_t l = 0; l < v.nl; ++l) {
         v.nin[l] = l == 0 ? D : HIDDEN;
@@ -285,7 +301,7 @@ static mlp_view mlp_layout(const ntco_desc* d, const double* params) {
     return v;
 }
 
-/* Affine layers with hardGELU after every layer but the last ("We do not use any
+/* Affine layers with hardGELU (or GELU, activation = 1) after every layer but the last ("We do not use any
  * activation function on the output of the last layer").           */
 static void mlp_forward_keep(const mlp_view* v, const double* X, double z[4][HIDDEN],
                              double h[4][HIDDEN], double* y) {
@@ -298,7 +314,7 @@ static void mlp_forward_keep(const mlp_view* v, const double* X, double z[4][HID
             out[o] = s;
         }
         if (l < v->nl - 1) {
-            for (int32_t o = 0; o < HIDDEN; ++o) h[l][o] = ntco_hardgelu(z[l][o]);
+            for (int32_t o = 0; o < HIDDEN; ++o) h[l][o] = act(v->act, z[l][o]);
             in = h[l];
         }
     }
@@ -543,7 +559,7 @@ double ntco_train_grads(const ntco_desc* d, const float* latents, const float* p
                 dh[i] = s;
             }
             if (l > 0)
-                for (int32_t i = 0; i < HIDDEN; ++i) dz[i] = dh[i] * ntco_hardgelu_grad(z[l - 1][i]);
+                for (int32_t i = 0; i < HIDDEN; ++i) dz[i] = dh[i] * act_grad(v.act, z[l - 1][i]);
         }
         for (int32_t i = 0; i < nlat_in; ++i) dX[t * nlat_in + i] = dh[i];
         (void)D;

@@ -37,7 +37,7 @@ typedef struct {
     int32_t c0, b0;       /* G_0 channels C_0 and bits B_0                      */
     int32_t c1, b1;       /* G_1 channels C_1 and bits B_1                      */
     int32_t hidden_mats;  /* 1: [D,64,64,c]  2: [D,64,64,64,c]  (R11)           */
-    int32_t activation;   /* 0: hardGELU                     */
+    int32_t activation;   /* 0: hardGELU, 1: exact GELU */
 } ntco_desc;
 
 /* ---- geometry / addressing (Table 1) ---- */
@@ -74,6 +74,8 @@ void     ntco_assemble(const ntco_desc* d, const uint8_t* codes, int32_t mip,
 /* ---- network ---- */
 double ntco_hardgelu(double x);
 double ntco_hardgelu_grad(double x);
+double ntco_gelu(double x);      /* exact GELU, activation = 1 */
+double ntco_gelu_grad(double x);
 /* params in ABI order (W1[64][D], b1[64], W2[64][64], b2[64], [W2b, b2b], W3[c][64], b3[c]) */
 void   ntco_mlp_forward(const ntco_desc* d, const double* params, const double* X, double* y);
 

@@ -62,7 +62,8 @@ static ntc_status check_desc(const ntc_desc* d) {
     if (d->b0 < 1 || d->b0 > 8 || d->b1 < 1 || d->b1 > 8 || d->c0 < 1 || d->c1 < 1)
         return fail(NTC_ERR_INVALID_ARGUMENT, "bad grid channels/bits");
     if (d->hidden_mats != 1 && d->hidden_mats != 2) return fail(NTC_ERR_INVALID_ARGUMENT, "hidden_mats must be 1 or 2");
-    if (d->activation != 0) return fail(NTC_ERR_UNSUPPORTED, "only hardGELU (activation 0) is compiled");
+    if (d->activation != 0 && d->activation != 1)
+        return fail(NTC_ERR_UNSUPPORTED, "activation must be 0 (hardGELU) or 1 (exact GELU)");
     if (profile_id(d) < 0) return fail(NTC_ERR_UNSUPPORTED, "profile (C0=%d,B0=%d,C1=%d,B1=%d) not compiled", d->c0, d->b0, d->c1, d->b1);
     return NTC_OK;
 }
@@ -330,6 +331,7 @@ DecodeParams ntc::base_params(const ntc_material* m) {
     p.wimg_bytes = m->wimg_bytes;
     p.W = m->d.width;
     p.c = m->d.channels;
+    p.act = m->d.activation;
     p.M = m->M;
     p.L = m->L;
     for (int j = 0; j < m->L; ++j) p.lv[j] = m->lv[j];

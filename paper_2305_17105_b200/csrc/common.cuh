@@ -44,6 +44,7 @@ struct DecodeParams {
     uint32_t wimg_bytes;
     int32_t W, c, M, L;
     int32_t mode;             // 0: tiles over mips, 1: queries, 2: debug assemble
+    int32_t act;              // 0: hardGELU, 1: exact GELU (selects the kernel instantiation)
     LevelGeom lv[MAX_LEVELS];
     int8_t level_of[MAX_MIPS];
     uint32_t lod_word[MAX_MIPS];  // half(lod) | half(1.0) << 16

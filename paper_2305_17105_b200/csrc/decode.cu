@@ -40,8 +40,24 @@ __device__ __forceinline__ uint32_t hardgelu2(uint32_t a, uint32_t b) {
     return pack_half2(h.x, h.y);
 }
 
+// exact GELU of a column pair: z Phi(z) = z/2 (1 + erf(z / sqrt 2)) (f4 variant)
+__device__ __forceinline__ uint32_t gelu2(uint32_t a, uint32_t b) {
+    const float za = __uint_as_float(a), zb = __uint_as_float(b);
+    return pack_half2(0.5f * za * (1.0f + erff(za * 0.70710678118654752f)),
+                      0.5f * zb * (1.0f + erff(zb * 0.70710678118654752f)));
+}
+
+template <int ACT>
+__device__ __forceinline__ uint32_t act2(uint32_t a, uint32_t b) {
+    if constexpr (ACT == 0)
+        return hardgelu2(a, b);
+    else
+        return gelu2(a, b);
+}
+
 // TMEM accumulator columns [0, 64) of this thread's lane (bias already accumulated)
-// -> hardGELU -> fp16 -> row `row` of the SW128 A tile, 32 columns at a time
+// -> hardGELU (or GELU) -> fp16 -> row `row` of the SW128 A tile, 32 columns at a time
+template <int ACT>
 __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, int row) {
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -50,7 +66,7 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, i
         tmem_wait_ld();
         uint32_t h[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) h[i] = hardgelu2(r[2 * i], r[2 * i + 1]);
+        for (int i = 0; i < 16; ++i) h[i] = act2<ACT>(r[2 * i], r[2 * i + 1]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int chunk = 4 * half + c;
@@ -166,7 +182,7 @@ struct Ctx {
     uint64_t adesc;     // SW128 K-major descriptor of abuf
 };
 
-template <class P, int HM, bool MULTI>
+template <class P, int HM, bool MULTI, int ACT>
 __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTable* mt) {
     using S = DecodeSmem<P, HM>;
     constexpr int NW = S::NWG;
@@ -277,7 +293,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         mbar_wait(C.bar, C.phase);
         C.phase ^= 1;
         tc_fence_after();
-        epilogue_hidden(C.tcol + lane_off, C.abuf, row);
+        epilogue_hidden<ACT>(C.tcol + lane_off, C.abuf, row);
         fence_proxy_async_smem();
         tc_fence_before();
         handoff(C);
@@ -370,15 +386,15 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-template <class P, int HM>
+template <class P, int HM, int ACT>
 __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
-    decode_body<P, HM, false>(p, nullptr);
+    decode_body<P, HM, false, ACT>(p, nullptr);
 }
 
-template <class P, int HM>
+template <class P, int HM, int ACT>
 __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1)
     decode_multi_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ MultiTable mt) {
-    decode_body<P, HM, true>(p, &mt);
+    decode_body<P, HM, true, ACT>(p, &mt);
 }
 
 // Tests only: the same addressing + assembly, written to global memory in canonical order.
@@ -462,6 +478,15 @@ static auto dispatch(int pid, int hm, F&& f) {
     }
 }
 
+// + the activation (0 hardGELU, 1 exact GELU) for the decode kernels
+template <class F>
+static auto dispatch_act(int pid, int hm, int act, F&& f) {
+    return dispatch(pid, hm, [&](auto pr, auto h) {
+        if (act == 1) return f(pr, h, std::integral_constant<int, 1>{});
+        return f(pr, h, std::integral_constant<int, 0>{});
+    });
+}
+
 uint32_t decode_wimg_bytes(int pid, int hm) {
     return dispatch(pid, hm, [](auto pr, auto h) { return DecodeSmem<decltype(pr), decltype(h)::value>::WIMG; });
 }
@@ -477,11 +502,11 @@ cudaError_t build_wimg(int pid, int hm, const uint16_t* w, int c, uint8_t* img, 
 }
 
 cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cudaStream_t s) {
-    return dispatch(pid, hm, [&](auto pr, auto h) {
+    return dispatch_act(pid, hm, p.act, [&](auto pr, auto h, auto a) {
         using PP = decltype(pr);
         constexpr int HMv = decltype(h)::value;
         using SS = DecodeSmem<PP, HMv>;
-        auto* k = decode_kernel<PP, HMv>;
+        auto* k = decode_kernel<PP, HMv, decltype(a)::value>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
         if (e != cudaSuccess) return e;
         k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p);
@@ -491,11 +516,11 @@ cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cuda
 
 cudaError_t launch_decode_multi(int pid, int hm, const DecodeParams& p, const MultiTable& mt, int grid,
                                 cudaStream_t s) {
-    return dispatch(pid, hm, [&](auto pr, auto h) {
+    return dispatch_act(pid, hm, p.act, [&](auto pr, auto h, auto a) {
         using PP = decltype(pr);
         constexpr int HMv = decltype(h)::value;
         using SS = DecodeSmem<PP, HMv>;
-        auto* k = decode_multi_kernel<PP, HMv>;
+        auto* k = decode_multi_kernel<PP, HMv, decltype(a)::value>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
         if (e != cudaSuccess) return e;
         k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p, mt);

@@ -202,7 +202,22 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
     p.grad_lat[li] = 0.0f;
 }
 
-template <int C0, int C1>
+// hidden activation and its derivative: hardGELU (R15) or exact GELU (f4):
+// x Phi(x) and Phi(x) + x phi(x)
+template <int ACT>
+__device__ __forceinline__ void act_and_grad(float z, float& h, float& g) {
+    if constexpr (ACT == 0) {
+        h = hgelu(z);
+        g = hgelu_d(z);
+    } else {
+        const float Phi = 0.5f * (1.0f + erff(z * 0.70710678118654752f));
+        const float phi = 0.39894228040143268f * expf(-0.5f * z * z);
+        h = z * Phi;
+        g = fmaf(z, phi, Phi);
+    }
+}
+
+template <int C0, int C1, int ACT>
 __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_constant__ TrainParams p) {
     using S = TrainSmem;
     constexpr int D = 4 * C0 + C1 + 13;
@@ -442,8 +457,11 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
                         z0 += bb.x;
                         z1 += bb.y;
                     }
-                    h[i] = h2u(hgelu(z0), hgelu(z1));
-                    g[i] = h2u(hgelu_d(z0), hgelu_d(z1));
+                    float h0, h1, g0, g1;
+                    act_and_grad<ACT>(z0, h0, g0);
+                    act_and_grad<ACT>(z1, h1, g1);
+                    h[i] = h2u(h0, h1);
+                    g[i] = h2u(g0, g1);
                 }
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
@@ -889,8 +907,9 @@ static int ilog2_t(int64_t v) {
 
 extern "C" ntc_status ntc_trainer_create(const ntc_desc* d, ntc_trainer** out) {
     if (!d || !out) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
-    if (!(d->c0 == 8 && d->b0 == 2 && d->c1 == 12 && d->b1 == 4) || d->hidden_mats != 1 || d->activation != 0)
-        return api_fail(NTC_ERR_UNSUPPORTED, "training kernel compiled for NTC 0.2, [D,64,64,c], hardGELU");
+    if (!(d->c0 == 8 && d->b0 == 2 && d->c1 == 12 && d->b1 == 4) || d->hidden_mats != 1 ||
+        (d->activation != 0 && d->activation != 1))
+        return api_fail(NTC_ERR_UNSUPPORTED, "training kernel compiled for NTC 0.2, [D,64,64,c], hardGELU or GELU");
     if (d->channels < 1 || d->channels > 16 || d->width < 8 || (d->width & (d->width - 1)) ||
         d->width > (1 << 15))
         return api_fail(NTC_ERR_INVALID_ARGUMENT, "bad texture dims");
@@ -1174,7 +1193,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.freeze = hp->freeze_latents;
         const int grid = (int)std::min<int64_t>(std::min<int64_t>(t->num_sms, 8 * RED_MAXK),
                                                 (tiles + TRAIN_WG - 1) / TRAIN_WG);
-        auto* k = train_kernel<8, 12>;
+        auto* k = d->activation == 1 ? train_kernel<8, 12, 1> : train_kernel<8, 12, 0>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TrainSmem::BYTES);
         if (e == cudaSuccess) {
             k<<<grid, TRAIN_WG * 128, TrainSmem::BYTES, st>>>(tp);

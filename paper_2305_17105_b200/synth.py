@@ -35,9 +35,9 @@ class Profile:
     activation: int = 0
 
     @staticmethod
-    def named(name: str, width: int, channels: int, hidden_mats: int = 1) -> "Profile":
+    def named(name: str, width: int, channels: int, hidden_mats: int = 1, activation: int = 0) -> "Profile":
         r, c0, b0, c1, b1 = PROFILES[name]
-        return Profile(width, channels, r, c0, b0, c1, b1, hidden_mats, 0)
+        return Profile(width, channels, r, c0, b0, c1, b1, hidden_mats, activation)
 
     @property
     def input_dim(self) -> int:  # PAPER.md:493 (shape bookkeeping only)

@@ -210,3 +210,26 @@ def test_full_size_4k_sampled(O):
     got = out.view(-1, 16)[torch.from_numpy(idx).to(DEV)].float().cpu().numpy()
     ref = O.decode_texels(d, codes, w, xym)
     assert np.abs(got - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("name,hm,c", [("ntc0.2", 1, 9), ("ntc0.2", 2, 8), ("ntc0.5", 1, 16), ("ntc2.25", 2, 12)])
+def test_decode_gelu_variant(O, name, hm, c):
+    """f4: exact GELU activation (activation = 1) -- full chain and random
+    queries vs the oracle, every compiled profile family, both depths."""
+    W = 128
+    d = Profile.named(name, W, c, hm, activation=1)
+    mat, codes, w = _material(O, d, 61 + hm)
+    T = ntc.ntc_chain_texels(d)
+    out = torch.full((T * c,), float("nan"), dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_chain(mat, out)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for m in range(O.num_mips(W)):
+        wm = W >> m
+        off = ntc.ntc_mip_offset(d, m) * c
+        err = np.abs(got[off: off + wm * wm * c] - O.decode_mip(d, codes, w, m).reshape(-1))
+        assert err.max() <= TOL, (m, err.max())
+    xym = gen_queries(5, W, 5000)
+    gq, st = _decode_queries_gpu(mat, xym)
+    assert st == 0
+    assert np.abs(gq - O.decode_texels(d, codes, w, xym)).max() <= TOL

@@ -17,8 +17,8 @@ DEV = "cuda:0"
 REL = 1e-2
 
 
-def _setup(O, W, c, seed, mip, n_crops, crop, out_gain=1.0):
-    d = Profile.named("ntc0.2", W, c)
+def _setup(O, W, c, seed, mip, n_crops, crop, out_gain=1.0, activation=0):
+    d = Profile.named("ntc0.2", W, c, activation=activation)
     lat = gen_latents(seed, O.num_latents(d))
     par = gen_weights_f32(seed + 1, d.input_dim, c, out_gain=out_gain)
     chain = box_mip_chain_u8(gen_reference_u8(seed + 2, W, c))
@@ -90,6 +90,17 @@ def test_train_grads_small(O, mip, n_crops, crop):
     d, lat, par, ref, crops = _setup(O, 64, 8, 10 + mip, mip, n_crops, crop)
     loss, gp, gl, _ = _gpu_grads(O, d, lat, par, ref, crops, mip, 77, 5)
     loss_o, dp, dl = O.train_grads(d, lat, par, mip, crops, ref, 77, 5)
+    assert abs(loss - loss_o) <= 1e-3 * loss_o
+    _check_all(O, d, gp, gl, dp, dl)
+
+
+@pytest.mark.parametrize("mip,n_crops,crop", [(0, 2, 32), (3, 2, 8)])
+def test_train_grads_gelu(O, mip, n_crops, crop):
+    """f4: the exact-GELU variant (activation = 1) of the training step: loss
+    and every gradient tensor vs the oracle."""
+    d, lat, par, ref, crops = _setup(O, 64, 9, 40 + mip, mip, n_crops, crop, activation=1)
+    loss, gp, gl, _ = _gpu_grads(O, d, lat, par, ref, crops, mip, 41, 2)
+    loss_o, dp, dl = O.train_grads(d, lat, par, mip, crops, ref, 41, 2)
     assert abs(loss - loss_o) <= 1e-3 * loss_o
     _check_all(O, d, gp, gl, dp, dl)
 

@@ -23,11 +23,12 @@ def _material(O, d, seed):
     return lat, par, chain
 
 
-@pytest.mark.parametrize("mip,hidden", [(0, 1), (1, 1), (4, 1), (0, 2)])
-def test_gradients_finite_difference(O, mip, hidden):
+@pytest.mark.parametrize("mip,hidden,act", [(0, 1, 0), (1, 1, 0), (4, 1, 0), (0, 2, 0), (0, 1, 1), (1, 2, 1)])
+def test_gradients_finite_difference(O, mip, hidden, act):
     """Analytic gradients vs central differences (exact-input mode, h = 1e-6): per-tensor
-    relative L2 error < 1e-4 on sampled weights and every touched latent sample."""
-    d = Profile.named("ntc0.2", 32, 3, hidden)
+    relative L2 error < 1e-4 on sampled weights and every touched latent sample; hardGELU
+    (act 0) and exact GELU (act 1, the f4 variant)."""
+    d = Profile.named("ntc0.2", 32, 3, hidden, act)
     lat, par, chain = _material(O, d, 100 + mip)
     ref = u8_to_f16_bits(chain[mip])
     crops = gen_crops(5, 32, mip, 2, crop=8)

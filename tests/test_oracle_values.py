@@ -165,12 +165,38 @@ def test_hardgelu_grad_finite_difference(O):
     assert O.hardgelu_grad(1.5) == 1.5 and O.hardgelu_grad(-1.5) == -0.5
 
 
+# ---------------------------------------------------------------- exact GELU (f4)
+def test_gelu_matches_torch(O):
+    """activation = 1 is GELU: torch's exact (erf) GELU and its autograd
+    derivative as the library routines."""
+    xs = torch.linspace(-6, 6, 2401, dtype=torch.float64, requires_grad=True)
+    ref = torch.nn.functional.gelu(xs, approximate="none")
+    (gref,) = torch.autograd.grad(ref.sum(), xs)
+    got = np.array([O.gelu(float(x)) for x in xs.detach()])
+    gg = np.array([O.gelu_grad(float(x)) for x in xs.detach()])
+    assert np.allclose(got, ref.detach().numpy(), atol=1e-14, rtol=0)
+    assert np.allclose(gg, gref.numpy(), atol=1e-13, rtol=0)
+
+
+def test_gelu_identities(O):
+    """x Phi(x) closed forms: GELU(0) = 0, GELU(x) - GELU(-x) = x (Phi(x) + Phi(-x) = 1),
+    GELU'(0) = 1/2, GELU'(x) + GELU'(-x) = 1, and GELU(x) -> x / 0 in the tails."""
+    assert O.gelu(0.0) == 0.0 and O.gelu_grad(0.0) == 0.5
+    for x in np.linspace(-5, 5, 101):
+        assert abs(O.gelu(x) - O.gelu(-x) - x) < 1e-14
+        assert abs(O.gelu_grad(x) + O.gelu_grad(-x) - 1.0) < 1e-14
+    assert abs(O.gelu(12.0) - 12.0) < 1e-15 and abs(O.gelu(-12.0)) < 1e-15
+    h = 1e-6
+    for x in np.linspace(-4, 4, 81):
+        assert abs((O.gelu(x + h) - O.gelu(x - h)) / (2 * h) - O.gelu_grad(x)) < 1e-8
+
+
 # ---------------------------------------------------------------- MLP
-@pytest.mark.parametrize("hidden_mats,c", [(1, 8), (1, 16), (2, 9)])
-def test_mlp_matches_torch(O, hidden_mats, c):
-    """Reduces to library routines: torch fp64 Linear layers + hardswish(2x)/2, no output
-    activation (PAPER.md:492-496)."""
-    d = Profile.named("ntc0.2", 64, c, hidden_mats)
+@pytest.mark.parametrize("hidden_mats,c,act", [(1, 8, 0), (1, 16, 0), (2, 9, 0), (1, 9, 1), (2, 8, 1)])
+def test_mlp_matches_torch(O, hidden_mats, c, act):
+    """Reduces to library routines: torch fp64 Linear layers + hardswish(2x)/2 (activation 0)
+    or exact GELU (activation 1), no output activation."""
+    d = Profile.named("ntc0.2", 64, c, hidden_mats, act)
     D = d.input_dim
     w = gen_weights_f16(11, D, c, hidden_mats).view(np.float16).astype(np.float64)
     rng = np.random.default_rng(1)
@@ -191,7 +217,7 @@ def test_mlp_matches_torch(O, hidden_mats, c):
         for i, lin in enumerate(layers):
             h = lin(h)
             if i < len(layers) - 1:
-                h = torch.nn.functional.hardswish(2 * h) / 2
+                h = torch.nn.functional.hardswish(2 * h) / 2 if act == 0 else torch.nn.functional.gelu(h)
     for i in range(X.shape[0]):
         y = O.mlp_forward(d, w, X[i])
         assert np.allclose(y, h[i].numpy(), atol=1e-12, rtol=0)
