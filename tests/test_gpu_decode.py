@@ -233,3 +233,43 @@ def test_decode_gelu_variant(O, name, hm, c):
     gq, st = _decode_queries_gpu(mat, xym)
     assert st == 0
     assert np.abs(gq - O.decode_texels(d, codes, w, xym)).max() <= TOL
+
+
+def test_bench_configs_sampled(O):
+    """The bench's own launch configurations at full size (bench.py): the 4096^2 9-ch chain
+    material of the headline line (seed base + 4) through one ntc_decode_chain launch, and the
+    `random` line's 2^24 area-uniform queries on the 4096^2 16-ch material through one
+    ntc_decode_texels launch; sampled rows vs the oracle."""
+    from paper_2305_17105_b200.synth import SEED_BASE, gen_codes, gen_weights_f16
+
+    rng = np.random.default_rng(123)
+    # headline: decode chain
+    d = Profile.named("ntc0.2", 4096, 9)
+    codes = gen_codes(SEED_BASE + 4, ntc.grid_list(d))
+    w = gen_weights_f16(SEED_BASE + 5, d.input_dim, 9)
+    mat = ntc.Material(d, torch.from_numpy(codes).to(DEV), torch.from_numpy(w.view(np.int16)).to(DEV))
+    T = ntc.ntc_chain_texels(d)
+    out = torch.empty((T, 9), dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_chain(mat, out)
+    torch.cuda.synchronize()
+    xym = gen_queries(21, 4096, 150000, "mip")
+    offs = np.array([ntc.ntc_mip_offset(d, m) for m in range(13)], np.int64)
+    idx = offs[xym[:, 2]] + xym[:, 1].astype(np.int64) * (4096 >> xym[:, 2]) + xym[:, 0]
+    got = out[torch.from_numpy(idx).to(DEV)].float().cpu().numpy()
+    assert np.abs(got - O.decode_texels(d, codes, w, xym)).max() <= TOL
+    del out, mat
+    # random line: 2^24 queries, 16 channels
+    d = Profile.named("ntc0.2", 4096, 16)
+    codes = gen_codes(SEED_BASE + 2, ntc.grid_list(d))
+    w = gen_weights_f16(SEED_BASE + 3, d.input_dim, 16)
+    mat = ntc.Material(d, torch.from_numpy(codes).to(DEV), torch.from_numpy(w.view(np.int16)).to(DEV))
+    n = 1 << 24
+    xym = gen_queries(SEED_BASE + 4, 4096, n, "area")
+    out = torch.empty((n, 16), dtype=torch.float16, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ntc.ntc_decode_texels(mat, ntc.pack_queries(torch.from_numpy(xym).to(DEV)), out, st)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    sel = rng.choice(n, 150000, replace=False)
+    got = out[torch.from_numpy(sel).to(DEV)].float().cpu().numpy()
+    assert np.abs(got - O.decode_texels(d, codes, w, xym[sel])).max() <= TOL

@@ -132,3 +132,24 @@ def test_multi_rejects_mixed_descs(O):
     out = torch.empty((4, 9), dtype=torch.float16, device=DEV)
     with pytest.raises(RuntimeError):
         ntc.ntc_decode_texels_multi(m1 + m2, q, out)
+
+
+def test_multi_bench_screen_workload_sampled(O):
+    """The bench's `multi` line at full size: the Table 4 analog (8,294,400 screen-order mip-0
+    queries, 8 materials of 4096^2 x 8 ch, one material per 64x64 screen block) in one
+    ntc_decode_texels_multi call; sampled rows vs the oracle decode of their material."""
+    import bench
+    from paper_2305_17105_b200.synth import SEED_BASE, gen_codes, gen_weights_f16
+
+    d = Profile.named("ntc0.2", 4096, 8)
+    mats, ins = [], []
+    for k in range(8):
+        codes = gen_codes(SEED_BASE + 4 + k, ntc.grid_list(d))
+        w = gen_weights_f16(SEED_BASE + 5 + k, d.input_dim, 8)
+        mats.append(ntc.Material(d, torch.from_numpy(codes).to(DEV), torch.from_numpy(w.view(np.int16)).to(DEV)))
+        ins.append((codes, w))
+    xym, mid = bench.screen_queries(8)
+    got_all, st = _run(mats, xym, mid)
+    assert st == 0
+    sel = np.random.default_rng(7).choice(xym.shape[0], 80000, replace=False)
+    _check(O, d, ins, xym[sel], mid[sel], got_all[sel])
