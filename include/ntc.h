@@ -249,6 +249,25 @@ ntc_status ntc_footprint_pack(const ntc_desc* d, const ntc_batch* batch, const f
 ntc_status ntc_footprint_unpack(const ntc_desc* d, const ntc_batch* batch, const float* packed, float* dst,
                                 ntc_stream stream);
 
+/* Explicit box lists, for the sharded data-parallel mode (multi-GPU: every rank
+ * owns a row band of every latent grid and its Adam state).  boxes: host int32 [n][6] in the
+ * ntc_train_footprint format (level, grid k, x0, y0, x1, y1), inclusive and disjoint,
+ * n <= 256; a box outside its grid -> NTC_ERR_INVALID_ARGUMENT.
+ * ntc_boxes_size: latent count covered (host, pure; -1 on bad boxes).
+ * ntc_boxes_copy (device fp32, box order, channel-minor within a cell):
+ *   NTC_BOX_PACK   dst[i] = src[latent i]            (dst packed, src canonical)
+ *   NTC_BOX_UNPACK dst[latent i] = src[i]            (src packed, dst canonical)
+ *   NTC_BOX_ADD    dst[latent i] += src[i]
+ *   NTC_BOX_ZERO   dst[latent i] = 0                 (src unused)
+ * ntc_train_apply_boxes: the APPLY phase of ntc_train_step (Adam on the weights, then on the
+ *   latents inside `boxes`, then the latent clamp) for an explicit box list.              */
+enum { NTC_BOX_PACK = 0, NTC_BOX_UNPACK = 1, NTC_BOX_ADD = 2, NTC_BOX_ZERO = 3 };
+int64_t ntc_boxes_size(const ntc_desc* d, const int32_t* boxes, int32_t n);
+ntc_status ntc_boxes_copy(const ntc_desc* d, const int32_t* boxes, int32_t n, const float* src, float* dst,
+                          int32_t mode, ntc_stream stream);
+ntc_status ntc_train_apply_boxes(ntc_trainer* t, const ntc_desc* d, const ntc_train_buffers* buf,
+                                 const int32_t* boxes, int32_t n, const ntc_train_hparams* hp, ntc_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,11 @@ ABI_FUNCTIONS = {
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                                ctypes.c_void_p]),
     "ntc_footprint_size": (ctypes.c_int64, [ctypes.c_void_p] * 2),
+    "ntc_boxes_size": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]),
+    "ntc_boxes_copy": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
+    "ntc_train_apply_boxes": (ctypes.c_int, [ctypes.c_void_p] * 4 + [ctypes.c_int32, ctypes.c_void_p,
+                                                                     ctypes.c_void_p]),
     "ntc_filter_scratch_bytes": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),
     "ntc_filter_texels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                          ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
@@ -359,6 +364,35 @@ def ntc_footprint_size(d, batch) -> int:
 def ntc_footprint_pack(d, batch, src: torch.Tensor, packed: torch.Tensor, stream=None):
     _check(lib().ntc_footprint_pack(ctypes.byref(make_desc(d)), ctypes.byref(_b(batch)), _ptr(src), _ptr(packed),
                                     _stream(stream)))
+
+
+NTC_BOX_PACK, NTC_BOX_UNPACK, NTC_BOX_ADD, NTC_BOX_ZERO = 0, 1, 2, 3
+
+
+def _boxes_arg(boxes):
+    import numpy as np
+
+    bx = np.ascontiguousarray(np.asarray(boxes, dtype=np.int32).reshape(-1, 6))
+    return bx, bx.ctypes.data_as(ctypes.c_void_p), bx.shape[0]
+
+
+def ntc_boxes_size(d, boxes) -> int:
+    bx, ptr, n = _boxes_arg(boxes)
+    v = lib().ntc_boxes_size(ctypes.byref(make_desc(d)), ptr, n)
+    if v < 0:
+        raise NtcError(NTC_ERR_INVALID_ARGUMENT, lib().ntc_last_error().decode())
+    return int(v)
+
+
+def ntc_boxes_copy(d, boxes, src, dst: torch.Tensor, mode: int, stream=None):
+    bx, ptr, n = _boxes_arg(boxes)
+    _check(lib().ntc_boxes_copy(ctypes.byref(make_desc(d)), ptr, n, _ptr(src), _ptr(dst), mode, _stream(stream)))
+
+
+def ntc_train_apply_boxes(trainer: Trainer, buffers: TrainBuffers, boxes, hp: Hparams, stream=None):
+    bx, ptr, n = _boxes_arg(boxes)
+    _check(lib().ntc_train_apply_boxes(trainer.handle, ctypes.byref(trainer.desc), ctypes.byref(buffers), ptr, n,
+                                       ctypes.byref(hp), _stream(stream)))
 
 
 def ntc_footprint_unpack(d, batch, packed, dst: torch.Tensor, stream=None):

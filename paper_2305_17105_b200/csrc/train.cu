@@ -1058,16 +1058,19 @@ static int32_t box_prefix(const std::vector<Box>& boxes, Box* dst, int32_t* star
     return (int32_t)acc;
 }
 
-// packed <-> dense copy over footprint boxes (data-parallel latent-gradient exchange)
+// packed <-> dense copy over footprint boxes (data-parallel latent exchanges):
+// mode 0 pack, 1 unpack (src NULL: zero), 2 unpack-add
 __global__ void footprint_copy_kernel(const __grid_constant__ PrepParams p, const float* __restrict__ src,
-                                      float* __restrict__ dst, int unpack) {
+                                      float* __restrict__ dst, int mode) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.box_start[p.nbox]) return;
     int b;
     int64_t li;
     box_locate(p.box, p.box_start, p.nbox, i, b, li);
-    if (unpack)
+    if (mode == 1)
         dst[li] = src ? src[i] : 0.0f;
+    else if (mode == 2)
+        dst[li] += src[i];
     else
         dst[i] = src[li];
 }
@@ -1103,6 +1106,67 @@ extern "C" ntc_status ntc_footprint_pack(const ntc_desc* d, const ntc_batch* bat
 extern "C" ntc_status ntc_footprint_unpack(const ntc_desc* d, const ntc_batch* batch, const float* packed,
                                            float* dst, ntc_stream stream) {
     return footprint_copy(d, batch, packed, dst, 1, stream);
+}
+
+// ---- explicit box lists (sharded data-parallel mode, DESIGN.md multi-GPU): [n][6] int32
+// (level, grid k, x0, y0, x1, y1) inclusive, disjoint
+static ntc_status boxes_from_abi(const ntc_desc* d, const int32_t* in, int32_t n, std::vector<Box>& out) {
+    if (!d || (n > 0 && !in)) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n < 0 || n > MAX_BOXES) return api_fail(NTC_ERR_INVALID_ARGUMENT, "box count out of range");
+    const int L = ntc_num_levels(d);
+    out.clear();
+    for (int i = 0; i < n; ++i) {
+        const int32_t* b = in + 6 * i;
+        if (b[0] < 0 || b[0] >= L || (b[1] != 0 && b[1] != 1)) return api_fail(NTC_ERR_INVALID_ARGUMENT, "bad box grid");
+        int32_t r[2];
+        int64_t off[2];
+        ntc_grid_layout(d, b[0], &r[0], &r[1], &off[0], &off[1]);
+        const int k = b[1];
+        if (b[2] < 0 || b[3] < 0 || b[2] > b[4] || b[3] > b[5] || b[4] >= r[k] || b[5] >= r[k])
+            return api_fail(NTC_ERR_INVALID_ARGUMENT, "box outside its grid");
+        out.push_back(Box{off[k], r[k], k ? d->c1 : d->c0, k ? d->b1 : d->b0, b[2], b[3], b[4], b[5]});
+    }
+    return NTC_OK;
+}
+
+extern "C" int64_t ntc_boxes_size(const ntc_desc* d, const int32_t* boxes, int32_t n) {
+    std::vector<Box> bx;
+    if (boxes_from_abi(d, boxes, n, bx) != NTC_OK) return -1;
+    int64_t acc = 0;
+    for (const Box& b : bx) acc += (int64_t)(b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1) * b.C;
+    return acc;
+}
+
+extern "C" ntc_status ntc_boxes_copy(const ntc_desc* d, const int32_t* boxes, int32_t n, const float* src,
+                                     float* dst, int32_t mode, ntc_stream stream) {
+    std::vector<Box> bx;
+    if (ntc_status s = boxes_from_abi(d, boxes, n, bx)) return s;
+    if (mode < NTC_BOX_PACK || mode > NTC_BOX_ZERO) return api_fail(NTC_ERR_INVALID_ARGUMENT, "bad mode");
+    if (!dst || (mode != NTC_BOX_ZERO && !src)) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+    PrepParams pp;
+    memset(&pp, 0, sizeof pp);
+    pp.nbox = (int32_t)bx.size();
+    const int32_t cnt = box_prefix(bx, pp.box, pp.box_start);
+    if (cnt == 0) return NTC_OK;
+    const int km = mode == NTC_BOX_PACK ? 0 : mode == NTC_BOX_ADD ? 2 : 1;
+    footprint_copy_kernel<<<(cnt + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        pp, mode == NTC_BOX_ZERO ? nullptr : src, dst, km);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? NTC_OK : api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
+}
+
+static ntc_status apply_step(const ntc_desc* d, const ntc_train_buffers* buf, const std::vector<Box>& boxes,
+                             const ntc_train_hparams* hp, cudaStream_t st);
+
+extern "C" ntc_status ntc_train_apply_boxes(ntc_trainer* t, const ntc_desc* d, const ntc_train_buffers* buf,
+                                            const int32_t* boxes, int32_t n, const ntc_train_hparams* hp,
+                                            ntc_stream stream) {
+    if (!t || !d || !buf || !hp) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (memcmp(&t->d, d, sizeof(ntc_desc)) != 0) return api_fail(NTC_ERR_INVALID_ARGUMENT, "desc != trainer desc");
+    if (hp->step < 1) return api_fail(NTC_ERR_INVALID_ARGUMENT, "step must be >= 1");
+    std::vector<Box> bx;
+    if (ntc_status s = boxes_from_abi(d, boxes, n, bx)) return s;
+    return apply_step(d, buf, bx, hp, (cudaStream_t)stream);
 }
 
 extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const ntc_train_buffers* buf,
@@ -1204,51 +1268,59 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         }
         if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
     }
-    if (flags & NTC_STEP_APPLY) {
-        if (!buf->latents || !buf->m_lat || !buf->v_lat || !buf->grad_lat || !buf->params || !buf->m_par ||
-            !buf->v_par || !buf->grad_par)
-            return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
-        AdamParams a;
-        memset(&a, 0, sizeof a);
-        a.nbox = (int32_t)boxes.size();
-        const int32_t n = box_prefix(boxes, a.box, a.box_start);
-        a.dense_latents = hp->dense_latent_adam;
-        a.n_latents = NL;
-        a.P = (int32_t)P;
-        a.params = buf->params;
-        a.m_par = buf->m_par;
-        a.v_par = buf->v_par;
-        a.grad_par = buf->grad_par;
-        a.latents = buf->latents;
-        a.m_lat = buf->m_lat;
-        a.v_lat = buf->v_lat;
-        a.grad_lat = buf->grad_lat;
-        a.lr_w = hp->lr_weight;
-        a.lr_l = hp->lr_latent;
-        a.freeze = hp->freeze_latents;
-        a.b1 = hp->beta1;
-        a.b2 = hp->beta2;
-        a.eps = hp->eps;
-        a.c1 = (float)(1.0 - std::pow((double)hp->beta1, (double)hp->step));
-        a.c2 = (float)(1.0 - std::pow((double)hp->beta2, (double)hp->step));
-        const int L = ntc_num_levels(d);
-        a.ngrid = 2 * L;
-        int64_t acc = 0;
-        for (int j = 0; j < L; ++j) {
-            int32_t r0, r1;
-            int64_t o0, o1;
-            ntc_grid_layout(d, j, &r0, &r1, &o0, &o1);
-            a.grid_start[2 * j] = o0;
-            a.grid_bits[2 * j] = d->b0;
-            a.grid_start[2 * j + 1] = o1;
-            a.grid_bits[2 * j + 1] = d->b1;
-            acc = o1 + (int64_t)r1 * r1 * d->c1;
-        }
-        a.grid_start[2 * L] = acc;
-        const int64_t total = P + (hp->freeze_latents ? 0 : (hp->dense_latent_adam ? NL : (int64_t)n));
-        adam_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
+    if (flags & NTC_STEP_APPLY) return apply_step(d, buf, boxes, hp, st);
+    return NTC_OK;
+}
+
+// t8: Adam on the weights (dense) and on the latents of `boxes` (footprint-sparse unless
+// dense_latent_adam), then the latent clamp
+static ntc_status apply_step(const ntc_desc* d, const ntc_train_buffers* buf, const std::vector<Box>& boxes,
+                             const ntc_train_hparams* hp, cudaStream_t st) {
+    const int64_t P = ntc_num_params(d), NL = ntc_num_latents(d);
+    cudaError_t e = cudaSuccess;
+    if (!buf->latents || !buf->m_lat || !buf->v_lat || !buf->grad_lat || !buf->params || !buf->m_par ||
+        !buf->v_par || !buf->grad_par)
+        return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+    AdamParams a;
+    memset(&a, 0, sizeof a);
+    a.nbox = (int32_t)boxes.size();
+    const int32_t n = box_prefix(boxes, a.box, a.box_start);
+    a.dense_latents = hp->dense_latent_adam;
+    a.n_latents = NL;
+    a.P = (int32_t)P;
+    a.params = buf->params;
+    a.m_par = buf->m_par;
+    a.v_par = buf->v_par;
+    a.grad_par = buf->grad_par;
+    a.latents = buf->latents;
+    a.m_lat = buf->m_lat;
+    a.v_lat = buf->v_lat;
+    a.grad_lat = buf->grad_lat;
+    a.lr_w = hp->lr_weight;
+    a.lr_l = hp->lr_latent;
+    a.freeze = hp->freeze_latents;
+    a.b1 = hp->beta1;
+    a.b2 = hp->beta2;
+    a.eps = hp->eps;
+    a.c1 = (float)(1.0 - std::pow((double)hp->beta1, (double)hp->step));
+    a.c2 = (float)(1.0 - std::pow((double)hp->beta2, (double)hp->step));
+    const int L = ntc_num_levels(d);
+    a.ngrid = 2 * L;
+    int64_t acc = 0;
+    for (int j = 0; j < L; ++j) {
+        int32_t r0, r1;
+        int64_t o0, o1;
+        ntc_grid_layout(d, j, &r0, &r1, &o0, &o1);
+        a.grid_start[2 * j] = o0;
+        a.grid_bits[2 * j] = d->b0;
+        a.grid_start[2 * j + 1] = o1;
+        a.grid_bits[2 * j + 1] = d->b1;
+        acc = o1 + (int64_t)r1 * r1 * d->c1;
     }
+    a.grid_start[2 * L] = acc;
+    const int64_t total = P + (hp->freeze_latents ? 0 : (hp->dense_latent_adam ? NL : (int64_t)n));
+    adam_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
     return NTC_OK;
 }

@@ -111,3 +111,68 @@ def test_dp_step_two_ranks_matches_single_batch():
         assert np.linalg.norm(dgp - gp) <= 1e-5 * np.linalg.norm(gp)
         assert np.linalg.norm(dgl - gl) <= 1e-5 * np.linalg.norm(gl)
     assert np.array_equal(res[0][4], res[1][4]) and np.array_equal(res[0][5], res[1][5])
+
+
+def _shard_worker(rank, world, port, q, steps):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2305_17105_b200 as ntc
+        from paper_2305_17105_b200.dist import ShardedDataParallelTrainer
+        from paper_2305_17105_b200.synth import gen_crops
+
+        d, lat, par, ref, _ = _setup()
+        tr = ShardedDataParallelTrainer(d, torch.from_numpy(lat).to(DEV), torch.from_numpy(par).to(DEV))
+        refd = torch.from_numpy(ref.view(np.int16)).to(DEV)
+        losses = []
+        for s in range(steps):
+            hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, s + 1, 7, 1, 0)
+            losses.append(float(tr.step(0, gen_crops(40 + s, 128, 0, 6, 32), refd, 128 * 8, hp).item()))
+        full = tr.gather_latents()
+        torch.cuda.synchronize()
+        q.put((rank, losses, tr.t["params"].cpu().numpy().copy(), full.cpu().numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_dp_matches_single_process():
+    """Latent grids sharded by row bands (2 ranks): after 3 GRADS+APPLY steps the gathered
+    latents and the weights equal single-process training on the same global batches (fp32
+    summation order only), and the two ranks agree."""
+    from paper_2305_17105_b200.synth import gen_crops
+
+    steps = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q, steps)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    d, lat, par, ref, _ = _setup()
+    NL, P = lat.size, par.size
+    t = {k: torch.zeros(NL, device=DEV) for k in ("m_lat", "v_lat", "grad_lat", "noisy")}
+    t.update({k: torch.zeros(P, device=DEV) for k in ("m_par", "v_par", "grad_par")})
+    t["latents"] = torch.from_numpy(lat.copy()).to(DEV)
+    t["params"] = torch.from_numpy(par.copy()).to(DEV)
+    refd = torch.from_numpy(ref.view(np.int16)).to(DEV)
+    tr, bufs, loss = ntc.Trainer(d), ntc.make_buffers(t), torch.zeros(1, device=DEV)
+    losses = []
+    for s in range(steps):
+        hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, s + 1, 7, 1, 0)
+        ntc.ntc_train_step(tr, bufs, ntc.make_batch(0, gen_crops(40 + s, 128, 0, 6, 32), refd, 128 * 8), hp, loss)
+        losses.append(float(loss.item()))
+    torch.cuda.synchronize()
+    ref_lat, ref_par = t["latents"].cpu().numpy(), t["params"].cpu().numpy()
+    for _, l, p, full in res:
+        assert np.allclose(l, losses, rtol=1e-5)
+        assert np.allclose(p, ref_par, rtol=1e-4, atol=1e-6)
+        assert np.allclose(full, ref_lat, rtol=1e-4, atol=1e-6)
+    assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
