@@ -218,11 +218,15 @@ __device__ __forceinline__ void act_and_grad(float z, float& h, float& g) {
 }
 
 template <int C0, int C1, int ACT>
-__global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_constant__ TrainParams p) {
+__global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_constant__ TrainParams p) {
+    // Two independent tile pipelines ("slots") per CTA, 8 warps each.  The 4 TMEM lane
+    // quarters of a 128-texel tile are served by two warps each that split the columns: half
+    // h = 0 owns columns [0, 32) of every 64-wide activation (and the G0 part of X / dX), half
+    // h = 1 columns [32, 64) (and the G1 / PE / LOD part, the reference texels, the loss).
     using S = TrainSmem;
     constexpr int D = 4 * C0 + C1 + 13;
     constexpr int NLAT = 4 * C0 + C1;   // latent columns of X
-    static_assert(D < 64 && NLAT <= 48, "training kernel: K1 = 64 profiles");
+    static_assert(D < 64 && NLAT <= 48 && 4 * C0 == 32, "training kernel: K1 = 64, 32 G0 columns");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::WEND + TRAIN_WG * S::WG_BYTES);
@@ -233,11 +237,11 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     int* s_ts = reinterpret_cast<int*>(s_crop + NTC_MAX_CROPS);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wg = warp >> 2, q = warp & 3, row = q * 32 + lane;
+    const int slot = warp >> 3, h = (warp >> 2) & 1, q = warp & 3, row = q * 32 + lane;
     const int c = p.c;
 
-    // ---- weight images (fp16, SW128 K-major, built once per step by the trailing blocks of prep_kernel); the
-    // same images serve the backward MMAs through MN-major descriptors (W^T without a copy)
+    // ---- weight images (fp16, SW128 K-major, built once per step by the trailing blocks of
+    // prep_kernel); the same images serve the backward MMAs through MN-major descriptors
     for (uint32_t i = tid; i < S::WEND / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.wimg) + i);
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
@@ -257,23 +261,23 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
     __syncthreads();
     tc_fence_after();
 
-    // TMEM per warpgroup: [0,128) dW-a accumulator, [128,144) dW-b, [192,256) scratch
-    const uint32_t tbase = *s_tmem + (uint32_t)wg * 256u;
+    // TMEM per slot: [0,128) dW-a accumulator, [128,144) dW-b, [192,256) scratch
+    const uint32_t tbase = *s_tmem + (uint32_t)slot * 256u;
     const uint32_t t_acc_a = tbase, t_acc_b = tbase + 128, t_s = tbase + 192;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t tiles = sbase + S::WEND + (uint32_t)wg * S::WG_BYTES;
+    const uint32_t tiles = sbase + S::WEND + (uint32_t)slot * S::WG_BYTES;
     const uint32_t tX = tiles + S::X * S::TILE, tH1 = tiles + S::H1 * S::TILE, tH2 = tiles + S::H2 * S::TILE;
     const uint32_t tG1 = tiles + S::G1 * S::TILE, tG2 = tiles + S::G2 * S::TILE, tD3 = tiles + S::D3 * S::TILE;
-    const bool issuer = q == ((wg * 2) & 3) && lane == 0;  // issuing warps on different SM sub-partitions
-    uint64_t* bar = &s_bar[wg];
-    uint64_t* bar2 = &s_bar[TRAIN_WG + wg];
+    const bool issuer = (warp & 7) == slot * 2 && lane == 0;  // the two issuers on different sub-partitions
+    uint64_t* bar = &s_bar[slot];
+    uint64_t* bar2 = &s_bar[TRAIN_WG + slot];
     uint32_t phase = 0, phase2 = 0;
     bool pending_w = false;  // weight-gradient MMAs of the previous tile in flight
-    auto sync_wg = [&]() {
+    auto sync_slot = [&]() {
         fence_proxy_async_smem();
         tc_fence_before();
-        named_bar_sync(1 + wg, 128);
+        named_bar_sync(1 + slot, 256);
     };
     auto wait_mma = [&]() {
         mbar_wait(bar, phase);
@@ -315,63 +319,75 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         t.y = cr.y + (t.valid ? li / cr.z : 0);
         return t;
     };
-    auto taps_of = [&](const Texel& t, int (&tx0)[2], int (&ty0)[2], int (&tx1)[2], int (&ty1)[2], uint32_t (&wq)[4]) {
-        const int xs = 2 * t.x + 1, ys = 2 * t.y + 1;
-        int nx = (xs << p.lr0) - (1 << lw), ny = (ys << p.lr0) - (1 << lw);
-        int i = nx >> (lw + 1), j = ny >> (lw + 1);
-        tx0[0] = max(i, 0);
-        tx0[1] = min(i + 1, p.r0 - 1);
-        ty0[0] = max(j, 0);
-        ty0[1] = min(j + 1, p.r0 - 1);
-        nx = (xs << p.lr1) - (1 << lw);
-        ny = (ys << p.lr1) - (1 << lw);
-        i = nx >> (lw + 1);
-        j = ny >> (lw + 1);
-        const int mask = (2 << lw) - 1;  // bilinear weights in 1/256 units (exact, see decode)
-        const uint32_t ax = (uint32_t)(((nx & mask) << 4) >> (lw + 1)), ay = (uint32_t)(((ny & mask) << 4) >> (lw + 1));
-        wq[0] = (16u - ax) * (16u - ay);
-        wq[1] = ax * (16u - ay);
-        wq[2] = (16u - ax) * ay;
-        wq[3] = ax * ay;
-        tx1[0] = max(i, 0);
-        tx1[1] = min(i + 1, p.r1 - 1);
-        ty1[0] = max(j, 0);
-        ty1[1] = min(j + 1, p.r1 - 1);
+    // G0 taps (half 0) / G1 taps and bilinear weights in 1/256 units (half 1)
+    auto taps_g0 = [&](const Texel& t, int (&tx)[2], int (&ty)[2]) {
+        const int nx = ((2 * t.x + 1) << p.lr0) - (1 << lw), ny = ((2 * t.y + 1) << p.lr0) - (1 << lw);
+        const int i = nx >> (lw + 1), j = ny >> (lw + 1);
+        tx[0] = max(i, 0);
+        tx[1] = min(i + 1, p.r0 - 1);
+        ty[0] = max(j, 0);
+        ty[1] = min(j + 1, p.r0 - 1);
     };
-    // ---- t2 fetch of one texel: fp16 noisy latents of the 8 taps + raw reference, issued one
-    // tile ahead so the loads overlap the previous tile's MMA chain
-    static_assert(C0 == 8 && C1 % 4 == 0, "fetch layout: 16-byte G0 cells, 8-byte-aligned G1 cells");
+    auto taps_g1 = [&](const Texel& t, int (&tx)[2], int (&ty)[2], uint32_t& ax, uint32_t& ay) {
+        const int nx = ((2 * t.x + 1) << p.lr1) - (1 << lw), ny = ((2 * t.y + 1) << p.lr1) - (1 << lw);
+        const int i = nx >> (lw + 1), j = ny >> (lw + 1);
+        const int mask = (2 << lw) - 1;  // exact, see decode
+        ax = (uint32_t)(((nx & mask) << 4) >> (lw + 1));
+        ay = (uint32_t)(((ny & mask) << 4) >> (lw + 1));
+        tx[0] = max(i, 0);
+        tx[1] = min(i + 1, p.r1 - 1);
+        ty[0] = max(j, 0);
+        ty[1] = min(j + 1, p.r1 - 1);
+    };
+    // ---- t2 fetch, one tile ahead: half 0 the four fp16 G0 cells (4 x 16 B), half 1 the four
+    // fp16 G1 cells (4 x 24 B) and the raw reference texel (one register array serves both)
+    static_assert(C0 == 8 && C1 == 12, "fetch layout: 16-byte G0 cells, 24-byte G1 cells");
     struct Fetch {
         Texel t;
-        uint4 g0[4];
-        uint2 g1[4][C1 / 4];
-        uint32_t wq[4];
-        uint32_t ref[8];
+        uint32_t v[24];    // h = 0: G0 taps (4 x uint4); h = 1: G1 taps (4 x 3 x uint2)
+        uint32_t ref[8];   // h = 1: reference channels (fp16 pairs)
     };
     auto fetch = [&](int tile, Fetch& f) {
         f.t = texel_of(tile);
-        int tx0[2], ty0[2], tx1[2], ty1[2];
-        taps_of(f.t, tx0, ty0, tx1, ty1, f.wq);
-        const __half* g0 = p.noisy + p.off0;
-        const __half* g1 = p.noisy + p.off1;
+        if (h == 0) {
+            int tx[2], ty[2];
+            taps_g0(f.t, tx, ty);
+            const __half* g0 = p.noisy + p.off0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            f.g0[t] = __ldg(reinterpret_cast<const uint4*>(g0 + (ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0));
-            const uint2* c1 = reinterpret_cast<const uint2*>(g1 + (ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1);
+            for (int t = 0; t < 4; ++t) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(g0 + (ty[t >> 1] * p.r0 + tx[t & 1]) * C0));
+                f.v[4 * t] = v.x;
+                f.v[4 * t + 1] = v.y;
+                f.v[4 * t + 2] = v.z;
+                f.v[4 * t + 3] = v.w;
+            }
+        } else {
+            int tx[2], ty[2];
+            uint32_t ax, ay;
+            taps_g1(f.t, tx, ty, ax, ay);
+            const __half* g1 = p.noisy + p.off1;
 #pragma unroll
-            for (int e = 0; e < C1 / 4; ++e) f.g1[t][e] = __ldg(c1 + e);
-        }
-        const uint16_t* rp = p.ref + (int64_t)f.t.y * p.ref_stride + (int64_t)f.t.x * c;
+            for (int t = 0; t < 4; ++t) {
+                const uint2* c1 = reinterpret_cast<const uint2*>(g1 + (ty[t >> 1] * p.r1 + tx[t & 1]) * C1);
 #pragma unroll
-        for (int o = 0; o < 8; ++o) {
-            uint16_t lo = 0, hi = 0;
-            if (2 * o < c) lo = __ldg(rp + 2 * o);
-            if (2 * o + 1 < c) hi = __ldg(rp + 2 * o + 1);
-            f.ref[o] = (uint32_t)lo | ((uint32_t)hi << 16);
+                for (int e = 0; e < 3; ++e) {
+                    const uint2 v = __ldg(c1 + e);
+                    f.v[6 * t + 2 * e] = v.x;
+                    f.v[6 * t + 2 * e + 1] = v.y;
+                }
+            }
+            const uint16_t* rp = p.ref + (int64_t)f.t.y * p.ref_stride + (int64_t)f.t.x * c;
+#pragma unroll
+            for (int o = 0; o < 8; ++o) {
+                uint16_t lo = 0, hi = 0;
+                if (2 * o < c) lo = __ldg(rp + 2 * o);
+                if (2 * o + 1 < c) hi = __ldg(rp + 2 * o + 1);
+                f.ref[o] = (uint32_t)lo | ((uint32_t)hi << 16);
+            }
         }
     };
 
-    int tile = blockIdx.x * TRAIN_WG + wg;
+    int tile = blockIdx.x * TRAIN_WG + slot;
     const int tstride = gridDim.x * TRAIN_WG;
     Fetch F;
     if (tile < p.n_tiles) fetch(tile, F);
@@ -381,36 +397,42 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         uint32_t rawref[8];
 #pragma unroll
         for (int o = 0; o < 8; ++o) rawref[o] = F.ref[o];
-        // ---- a2-a4: X row (canonical column order, R4) -> SW128 tile
+        // ---- a2-a4: this half's 32 columns of the X row (canonical order, R4) -> SW128 tile
         {
-            uint32_t xw[32];
+            uint32_t xw[16];
+            if (h == 0) {  // G0 taps: the fp16 noisy latents are X
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {  // G0 taps: the fp16 noisy latents are X
-                xw[4 * t + 0] = F.g0[t].x;
-                xw[4 * t + 1] = F.g0[t].y;
-                xw[4 * t + 2] = F.g0[t].z;
-                xw[4 * t + 3] = F.g0[t].w;
-            }
-            {  // G1 bilinear in fp32 from the fp16 taps, rounded once
+                for (int i = 0; i < 16; ++i) xw[i] = F.v[i];
+            } else {       // G1 bilinear in fp32 from the fp16 taps, rounded once; PE; LOD
+                int tx[2], ty[2];
+                uint32_t ax, ay;
+                taps_g1(T, tx, ty, ax, ay);
+                const uint32_t wq[4] = {(16u - ax) * (16u - ay), ax * (16u - ay), (16u - ax) * ay, ax * ay};
                 float acc[C1];
 #pragma unroll
                 for (int e = 0; e < C1; ++e) acc[e] = 0.0f;
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const float wf = (float)F.wq[t] * (1.0f / 256.0f);
+                    const float wf = (float)wq[t] * (1.0f / 256.0f);
 #pragma unroll
-                    for (int e = 0; e < C1 / 4; ++e) {
-                        const uint2 v = F.g1[t][e];
-                        const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
-                        const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
-                        acc[4 * e + 0] = fmaf(wf, a0.x, acc[4 * e + 0]);
-                        acc[4 * e + 1] = fmaf(wf, a0.y, acc[4 * e + 1]);
-                        acc[4 * e + 2] = fmaf(wf, a1.x, acc[4 * e + 2]);
-                        acc[4 * e + 3] = fmaf(wf, a1.y, acc[4 * e + 3]);
+                    for (int e = 0; e < C1 / 2; ++e) {
+                        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&F.v[6 * t + e]));
+                        acc[2 * e + 0] = fmaf(wf, a.x, acc[2 * e + 0]);
+                        acc[2 * e + 1] = fmaf(wf, a.y, acc[2 * e + 1]);
                     }
                 }
 #pragma unroll
-                for (int e = 0; e < C1; e += 2) xw[(4 * C0 + e) / 2] = h2u(acc[e], acc[e + 1]);
+                for (int e = 0; e < C1; e += 2) xw[e / 2] = h2u(acc[e], acc[e + 1]);
+                constexpr int PEW = NLAT / 2 - 16;  // word index inside this half
+                xw[PEW + 0] = s_pe[4 * (T.x & 7) + 0];
+                xw[PEW + 1] = s_pe[4 * (T.x & 7) + 1];
+                xw[PEW + 2] = s_pe[4 * (T.x & 7) + 2];
+                xw[PEW + 3] = s_pe[4 * (T.y & 7) + 0];
+                xw[PEW + 4] = s_pe[4 * (T.y & 7) + 1];
+                xw[PEW + 5] = s_pe[4 * (T.y & 7) + 2];
+                xw[PEW + 6] = p.lod_word;
+#pragma unroll
+                for (int e = PEW + 7; e < 16; ++e) xw[e] = 0u;
             }
             if (pending_w) {  // the previous tile's weight-gradient MMAs still read the tiles
                 mbar_wait(bar2, phase2);
@@ -418,21 +440,11 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
                 tc_fence_after();
                 pending_w = false;
             }
-            constexpr int PEW = NLAT / 2;
-            xw[PEW + 0] = s_pe[4 * (T.x & 7) + 0];
-            xw[PEW + 1] = s_pe[4 * (T.x & 7) + 1];
-            xw[PEW + 2] = s_pe[4 * (T.x & 7) + 2];
-            xw[PEW + 3] = s_pe[4 * (T.y & 7) + 0];
-            xw[PEW + 4] = s_pe[4 * (T.y & 7) + 1];
-            xw[PEW + 5] = s_pe[4 * (T.y & 7) + 2];
-            xw[PEW + 6] = p.lod_word;
 #pragma unroll
-            for (int e = PEW + 7; e < 32; ++e) xw[e] = 0u;
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch)
-                sts_row_chunk(tX, row, ch, xw[4 * ch], xw[4 * ch + 1], xw[4 * ch + 2], xw[4 * ch + 3]);
+            for (int ch = 0; ch < 4; ++ch)
+                sts_row_chunk(tX, row, 4 * h + ch, xw[4 * ch], xw[4 * ch + 1], xw[4 * ch + 2], xw[4 * ch + 3]);
         }
-        sync_wg();
+        sync_slot();
         // ---- t3: forward.  Z1 = X W1^T (+b1)
         if (issuer) {
             tc_fence_after();
@@ -443,36 +455,33 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         if (tile + tstride < p.n_tiles) fetch(tile + tstride, F);  // next tile's loads in flight
         wait_mma();
         auto hidden_epilogue = [&](uint32_t tH, uint32_t tG, bool bias) {
+            uint32_t r[32];
+            tmem_ld32(t_s + lane_off + 32 * h, r);
+            tmem_wait_ld();
+            uint32_t hv[16], gv[16];
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint32_t r[32];
-                tmem_ld32(t_s + lane_off + 32 * half, r);
-                tmem_wait_ld();
-                uint32_t h[16], g[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
-                    if (bias) {
-                        const float2 bb = *reinterpret_cast<const float2*>(s_bias + 32 * half + 2 * i);
-                        z0 += bb.x;
-                        z1 += bb.y;
-                    }
-                    float h0, h1, g0, g1;
-                    act_and_grad<ACT>(z0, h0, g0);
-                    act_and_grad<ACT>(z1, h1, g1);
-                    h[i] = h2u(h0, h1);
-                    g[i] = h2u(g0, g1);
+            for (int i = 0; i < 16; ++i) {
+                float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
+                if (bias) {
+                    const float2 bb = *reinterpret_cast<const float2*>(s_bias + 32 * h + 2 * i);
+                    z0 += bb.x;
+                    z1 += bb.y;
                 }
+                float h0, h1, g0, g1;
+                act_and_grad<ACT>(z0, h0, g0);
+                act_and_grad<ACT>(z1, h1, g1);
+                hv[i] = h2u(h0, h1);
+                gv[i] = h2u(g0, g1);
+            }
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    sts_row_chunk(tH, row, 4 * half + cc, h[4 * cc], h[4 * cc + 1], h[4 * cc + 2], h[4 * cc + 3]);
-                    sts_row_chunk(tG, row, 4 * half + cc, g[4 * cc], g[4 * cc + 1], g[4 * cc + 2], g[4 * cc + 3]);
-                }
+            for (int cc = 0; cc < 4; ++cc) {
+                sts_row_chunk(tH, row, 4 * h + cc, hv[4 * cc], hv[4 * cc + 1], hv[4 * cc + 2], hv[4 * cc + 3]);
+                sts_row_chunk(tG, row, 4 * h + cc, gv[4 * cc], gv[4 * cc + 1], gv[4 * cc + 2], gv[4 * cc + 3]);
             }
         };
         hidden_epilogue(tH1, tG1, false);
-        sync_wg();
-        // Z2 = H1 W2^T + b2 (bias through X's constant column)
+        sync_slot();
+        // Z2 = H1 W2^T + b2
         if (issuer) {
             tc_fence_after();
 #pragma unroll
@@ -481,7 +490,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         }
         wait_mma();
         hidden_epilogue(tH2, tG2, true);
-        sync_wg();
+        sync_slot();
         // Y = H2 W3^T + b3
         if (issuer) {
             tc_fence_after();
@@ -490,8 +499,9 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
             mma_commit(bar);
         }
         wait_mma();
-        // ---- t4: mean-L2 loss (R17); delta3 = 2 (y - R) fed unscaled, 1/(B c) applied in fp32
-        {
+        // ---- t4: mean-L2 loss (R17) on half 1 (it holds the reference); delta3 = 2 (y - R)
+        // fed unscaled, 1/(B c) applied in fp32
+        if (h == 1) {
             uint32_t r[16];
             tmem_ld16(t_s + lane_off, r);
             tmem_wait_ld();
@@ -499,7 +509,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
 #pragma unroll
             for (int o = 0; o < 16; ++o) {
                 float rf;
-                asm volatile("{\n\t.reg .f16 h;\n\tmov.b16 h, %1;\n\tcvt.f32.f16 %0, h;\n\t}" : "=f"(rf)
+                asm volatile("{\n\t.reg .f16 hh;\n\tmov.b16 hh, %1;\n\tcvt.f32.f16 %0, hh;\n\t}" : "=f"(rf)
                              : "h"((uint16_t)(rawref[o >> 1] >> (16 * (o & 1)))));
                 const float e = (valid && o < c) ? __uint_as_float(r[o]) + s_bias[HID + o] - rf : 0.0f;
                 loss_acc = fmaf(e, e, loss_acc);
@@ -509,40 +519,37 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
             sts_row_chunk(tD3, row, 1, h2u(d3[8], d3[9]), h2u(d3[10], d3[11]), h2u(d3[12], d3[13]),
                           h2u(d3[14], d3[15]));
         }
-        sync_wg();
-        // ---- t5: dH2 = d3 W3 ; dW3/db3 += [X^T; H2^T] d3 (stacked, N = 16)
+        sync_slot();
+        // ---- t5: dH2 = d3 W3
         if (issuer) {
             tc_fence_after();
             mma_f16_ss(t_s, dD3, mW3, ID64_BT, 0);
             mma_commit(bar);
         }
         wait_mma();
-        auto delta_epilogue = [&](uint32_t tG) {  // delta = dH (TMEM) * hardGELU'(Z) (SMEM), in place
+        auto delta_epilogue = [&](uint32_t tG) {  // delta = fp16(dH) * hardGELU'(Z), in place
+            uint32_t r[32];
+            tmem_ld32(t_s + lane_off + 32 * h, r);
+            tmem_wait_ld();
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint32_t r[32];
-                tmem_ld32(t_s + lane_off + 32 * half, r);
-                tmem_wait_ld();
+            for (int cc = 0; cc < 4; ++cc) {
+                const uint4 gq = lds_row_chunk(tG, row, 4 * h + cc);
+                const uint32_t gw[4] = {gq.x, gq.y, gq.z, gq.w};
+                uint32_t o[4];
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    const uint4 gv = lds_row_chunk(tG, row, 4 * half + cc);
-                    const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
-                    uint32_t o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {  // delta = fp16(dA) * g' in packed fp16
-                        const __half2 g2 = *reinterpret_cast<const __half2*>(&gw[e]);
-                        const int col = 8 * cc + 2 * e;
-                        const uint32_t aw = h2u(__uint_as_float(r[col]), __uint_as_float(r[col + 1]));
-                        const __half2 dv = __hmul2(*reinterpret_cast<const __half2*>(&aw), g2);
-                        o[e] = *reinterpret_cast<const uint32_t*>(&dv);
-                    }
-                    sts_row_chunk(tG, row, 4 * half + cc, o[0], o[1], o[2], o[3]);
+                for (int e = 0; e < 4; ++e) {
+                    const __half2 g2 = *reinterpret_cast<const __half2*>(&gw[e]);
+                    const int col = 8 * cc + 2 * e;
+                    const uint32_t aw = h2u(__uint_as_float(r[col]), __uint_as_float(r[col + 1]));
+                    const __half2 dv = __hmul2(*reinterpret_cast<const __half2*>(&aw), g2);
+                    o[e] = *reinterpret_cast<const uint32_t*>(&dv);
                 }
+                sts_row_chunk(tG, row, 4 * h + cc, o[0], o[1], o[2], o[3]);
             }
         };
         delta_epilogue(tG2);  // G2 tile now holds delta2
-        sync_wg();
-        // dH1 = d2 W2 ; dW2/db2 += [X^T; H1^T] d2
+        sync_slot();
+        // dH1 = d2 W2
         if (issuer) {
             tc_fence_after();
 #pragma unroll
@@ -552,8 +559,8 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         }
         wait_mma();
         delta_epilogue(tG1);  // G1 tile now holds delta1
-        sync_wg();
-        // dX = d1 W1 (latent columns) ; dW1/db1 += [X^T; H1^T] d1
+        sync_slot();
+        // dX = d1 W1 (latent columns) ; weight gradients accumulated in TMEM
         if (issuer) {
             tc_fence_after();
 #pragma unroll
@@ -579,80 +586,40 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         wait_mma();
         first = false;
         pending_w = true;
-        // ---- t7: latent-gradient scatter: G0 taps unweighted, G1 taps bilinear-weighted
+        // ---- t7: latent-gradient scatter: half 0 the G0 taps (unweighted), half 1 the G1 taps
+        // (bilinear-weighted).  Neighbouring texels share tap cells (runs of 4 texels share all
+        // four G0 cells and runs of 8 share the G1 cells at LOD 0), so each run is summed to its
+        // first lane with two (G0) / three (G1) shuffle steps and only run heads issue the
+        // vector reductions -- no global contention storm.
         {
-            uint32_t r[48];
-            {
-                uint32_t a[32], b[16];
-                tmem_ld32(t_s + lane_off, a);
-                tmem_ld16(t_s + lane_off + 32, b);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) r[i] = a[i];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) r[32 + i] = b[i];
-            }
-            // Pre-reduce in the warp: neighbouring texels share tap cells (runs of 4 texels
-            // share all four G0 cells and runs of 8 share the G1 cells at LOD 0), so each run
-            // is summed to its first lane with two (G0) / three (G1) shuffle steps and only run
-            // heads issue the vector reductions -- no global contention storm.
-            int tx0[2], ty0[2], tx1[2], ty1[2];
-            uint32_t wq[4];
-            taps_of(T, tx0, ty0, tx1, ty1, wq);
             const float s = p.inv_bc;
-            float* gl0 = p.grad_lat + p.off0;
-            float* gl1 = p.grad_lat + p.off1;
             const bool on = valid && !(p.debug_flags & 1) && !p.freeze;
-            // run keys (invalid lanes get unique keys and never merge)
-            const uint32_t kx0 = on ? (uint32_t)(tx0[0] | (tx0[1] << 16)) : 0xFFFFFFF0u - lane;
-            const uint32_t ky0 = (uint32_t)(ty0[0] | (ty0[1] << 16));
-            const uint32_t kx1 = on ? (uint32_t)(tx1[0] | (tx1[1] << 16)) : 0xFFFFFFF0u - lane;
-            const uint32_t ky1 = (uint32_t)T.y;  // same y => same y-weights within a G1 run
-            const uint32_t ky1b = (uint32_t)(ty1[0] | (ty1[1] << 16));
-            // G0: 32 values (tap-major), unweighted
-            float g0v[32];
+            if (h == 0) {
+                uint32_t r[32];
+                tmem_ld32(t_s + lane_off, r);
+                tmem_wait_ld();
+                int tx0[2], ty0[2];
+                taps_g0(T, tx0, ty0);
+                float* gl0 = p.grad_lat + p.off0;
+                const uint32_t kx0 = on ? (uint32_t)(tx0[0] | (tx0[1] << 16)) : 0xFFFFFFF0u - lane;
+                const uint32_t ky0 = (uint32_t)(ty0[0] | (ty0[1] << 16));
+                float g0v[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) g0v[i] = on ? __uint_as_float(r[i]) : 0.0f;
-            // G1: per x-tap a, S_a = sum over the run of wx_a * dX_G1 (wy is constant in a run)
-            const float ax = (float)(wq[1] + wq[3]) * (1.0f / 256.0f);  // x-weight of tap column 1
-            const float ay = (float)(wq[2] + wq[3]) * (1.0f / 256.0f);  // y-weight of tap row 1
-            float g1v[2 * C1];
+                for (int i = 0; i < 32; ++i) g0v[i] = on ? __uint_as_float(r[i]) : 0.0f;
 #pragma unroll
-            for (int e = 0; e < C1; ++e) {
-                const float v = on ? __uint_as_float(r[4 * C0 + e]) : 0.0f;
-                g1v[e] = (1.0f - ax) * v;
-                g1v[C1 + e] = ax * v;
-            }
-#pragma unroll
-            for (int d = 1; d <= 4; d <<= 1) {
-                const uint32_t nx0 = __shfl_down_sync(0xffffffffu, kx0, d), ny0 = __shfl_down_sync(0xffffffffu, ky0, d);
-                const uint32_t nx1 = __shfl_down_sync(0xffffffffu, kx1, d), ny1 = __shfl_down_sync(0xffffffffu, ky1, d);
-                const uint32_t ny1b = __shfl_down_sync(0xffffffffu, ky1b, d);
-                const bool in = lane + d < 32;
-                const bool s0 = in && nx0 == kx0 && ny0 == ky0 && d < 4;
-                const bool s1 = in && nx1 == kx1 && ny1 == ky1 && ny1b == ky1b;
-                if (d < 4) {
+                for (int d = 1; d <= 2; d <<= 1) {
+                    const uint32_t nx0 = __shfl_down_sync(0xffffffffu, kx0, d);
+                    const uint32_t ny0 = __shfl_down_sync(0xffffffffu, ky0, d);
+                    const bool s0 = lane + d < 32 && nx0 == kx0 && ny0 == ky0;
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const float o = __shfl_down_sync(0xffffffffu, g0v[i], d);
                         if (s0) g0v[i] += o;
                     }
                 }
-#pragma unroll
-                for (int i = 0; i < 2 * C1; ++i) {
-                    const float o = __shfl_down_sync(0xffffffffu, g1v[i], d);
-                    if (s1) g1v[i] += o;
-                }
-            }
-            const uint32_t px0 = __shfl_up_sync(0xffffffffu, kx0, 1), py0 = __shfl_up_sync(0xffffffffu, ky0, 1);
-            const uint32_t px1 = __shfl_up_sync(0xffffffffu, kx1, 1), py1 = __shfl_up_sync(0xffffffffu, ky1, 1);
-            const uint32_t py1b = __shfl_up_sync(0xffffffffu, ky1b, 1);
-            // run heads; runs never exceed 4 (G0) / 8 (G1) lanes since r0/w_m >= 1/4 and
-            // r1/w_m >= 1/8 for the compiled profiles, which the 2 / 3 steps cover
-            const bool head1 = lane == 0 || px1 != kx1 || py1 != ky1 || py1b != ky1b;
-            if (on) {
-                const bool h0 = lane == 0 || px0 != kx0 || py0 != ky0;
-                if (h0) {
+                const uint32_t px0 = __shfl_up_sync(0xffffffffu, kx0, 1), py0 = __shfl_up_sync(0xffffffffu, ky0, 1);
+                // runs never exceed 4 lanes (r0 / w_m >= 1/4 for the compiled profiles)
+                if (on && (lane == 0 || px0 != kx0 || py0 != ky0)) {
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         float* dst = gl0 + ((int64_t)ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0;
@@ -662,17 +629,53 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
                                        s * g0v[t * C0 + e + 3]);
                     }
                 }
-                if (head1) {
+            } else {
+                uint32_t r[16];
+                tmem_ld16(t_s + lane_off + 32, r);
+                tmem_wait_ld();
+                int tx1[2], ty1[2];
+                uint32_t axq, ayq;
+                taps_g1(T, tx1, ty1, axq, ayq);
+                float* gl1 = p.grad_lat + p.off1;
+                const uint32_t kx1 = on ? (uint32_t)(tx1[0] | (tx1[1] << 16)) : 0xFFFFFFF0u - lane;
+                const uint32_t ky1 = (uint32_t)T.y;  // same y => same y-weights within a G1 run
+                const uint32_t ky1b = (uint32_t)(ty1[0] | (ty1[1] << 16));
+                // per x-tap a, S_a = sum over the run of wx_a * dX_G1 (wy is constant in a run)
+                const float ax = (float)axq * (1.0f / 16.0f);  // x-weight of tap column 1
+                const float ay = (float)ayq * (1.0f / 16.0f);  // y-weight of tap row 1
+                float g1v[2 * C1];
+#pragma unroll
+                for (int e = 0; e < C1; ++e) {
+                    const float v = on ? __uint_as_float(r[e]) : 0.0f;
+                    g1v[e] = (1.0f - ax) * v;
+                    g1v[C1 + e] = ax * v;
+                }
+#pragma unroll
+                for (int d = 1; d <= 4; d <<= 1) {
+                    const uint32_t nx1 = __shfl_down_sync(0xffffffffu, kx1, d);
+                    const uint32_t ny1 = __shfl_down_sync(0xffffffffu, ky1, d);
+                    const uint32_t ny1b = __shfl_down_sync(0xffffffffu, ky1b, d);
+                    const bool s1 = lane + d < 32 && nx1 == kx1 && ny1 == ky1 && ny1b == ky1b;
+#pragma unroll
+                    for (int i = 0; i < 2 * C1; ++i) {
+                        const float o = __shfl_down_sync(0xffffffffu, g1v[i], d);
+                        if (s1) g1v[i] += o;
+                    }
+                }
+                const uint32_t px1 = __shfl_up_sync(0xffffffffu, kx1, 1), py1 = __shfl_up_sync(0xffffffffu, ky1, 1);
+                const uint32_t py1b = __shfl_up_sync(0xffffffffu, ky1b, 1);
+                // runs never exceed 8 lanes (r1 / w_m >= 1/8)
+                if (on && (lane == 0 || px1 != kx1 || py1 != ky1 || py1b != ky1b)) {
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         const float wy = (t >> 1) ? ay : 1.0f - ay;
-                        const float* S = g1v + (t & 1) * C1;
+                        const float* Sv = g1v + (t & 1) * C1;
                         float* dst = gl1 + ((int64_t)ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1;
                         const float sw = s * wy;
                         if (sw != 0.0f) {
 #pragma unroll
                             for (int e = 0; e < C1; e += 4)
-                                red_add_v4(dst + e, sw * S[e], sw * S[e + 1], sw * S[e + 2], sw * S[e + 3]);
+                                red_add_v4(dst + e, sw * Sv[e], sw * Sv[e + 1], sw * Sv[e + 2], sw * Sv[e + 3]);
                         }
                     }
                 }
@@ -686,16 +689,18 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         phase2 ^= 1;
         tc_fence_after();
     }
-    // ---- t6: the CTA's weight-gradient partial (unscaled, one per CTA, fixed order): warpgroup
-    // 1 parks its TMEM accumulators in the (now idle) SMEM tile area, warpgroup 0 adds its own
-    // and writes the partial
+    // ---- t6: the CTA's weight-gradient partial (unscaled, one per CTA, fixed order): slot 1
+    // parks its TMEM accumulators in the (now idle) SMEM tile area, slot 0 adds its own and
+    // writes the partial.  Half 0 handles the dW1/db1 columns [0, 64), half 1 the dW2/db2
+    // columns [64, 128) and the dW3/db3 accumulator.
     float* part = p.partial + (size_t)blockIdx.x * p.P;
     float* park = reinterpret_cast<float*>(smem + S::WEND) + row * 145;  // [128][144] (+1 pad)
-    auto read_acc = [&](float (&v)[144], bool have) {
+    constexpr int NV = 80;  // values per thread: half 0 uses 64, half 1 uses 64 + 16
+    auto read_acc = [&](float (&v)[NV], bool have) {
 #pragma unroll
-        for (int blk = 0; blk < 4; ++blk) {
+        for (int blk = 0; blk < 2; ++blk) {
             uint32_t r[32];
-            tmem_ld32(t_acc_a + lane_off + 32 * blk, r);
+            tmem_ld32(t_acc_a + lane_off + 64 * h + 32 * blk, r);
             tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[32 * blk + e] = have ? __uint_as_float(r[e]) : 0.0f;
@@ -704,50 +709,58 @@ __global__ void __launch_bounds__(TRAIN_WG * 128, 1) train_kernel(const __grid_c
         tmem_ld16(t_acc_b + lane_off, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int o = 0; o < 16; ++o) v[128 + o] = have ? __uint_as_float(r[o]) : 0.0f;
+        for (int o = 0; o < 16; ++o) v[64 + o] = (have && h == 1) ? __uint_as_float(r[o]) : 0.0f;
     };
-    __syncthreads();  // both warpgroups are done with their tiles before the area is reused
-    if (wg == 1) {
-        float v[144];
+    __syncthreads();  // both slots are done with their tiles before the area is reused
+    if (slot == 1) {
+        float v[NV];
         read_acc(v, !first);
 #pragma unroll
-        for (int e = 0; e < 144; ++e) park[e] = v[e];
+        for (int e = 0; e < 64; ++e) park[64 * h + e] = v[e];
+        if (h == 1) {
+#pragma unroll
+            for (int o = 0; o < 16; ++o) park[128 + o] = v[64 + o];
+        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (wg == 0) {
-        float v[144];
+    if (slot == 0) {
+        float v[NV];
         read_acc(v, !first);
 #pragma unroll
-        for (int e = 0; e < 144; ++e) v[e] += park[e];
+        for (int e = 0; e < 64; ++e) v[e] += park[64 * h + e];
+        if (h == 1) {
+#pragma unroll
+            for (int o = 0; o < 16; ++o) v[64 + o] += park[128 + o];
+        }
         const int P1 = D * HID, o2 = P1 + HID, o3 = o2 + HID * HID + HID;
         const int m = row;  // stacked rows: [0,64) X features, [64,128) H units
+        if (h == 0) {
 #pragma unroll
-        for (int col = 0; col < 128; ++col) {
-            if (m < 64) {
-                if (col < 64) {
-                    if (m < D) part[col * D + m] = v[col];           // dW1[j][i]
-                    else if (m == D) part[P1 + col] = v[col];        // db1[j]
-                } else if (m == D) {
-                    part[o2 + HID * HID + (col - 64)] = v[col];      // db2[j]
-                }
-            } else if (col >= 64) {
-                part[o2 + (col - 64) * HID + (m - 64)] = v[col];     // dW2[j][i]
+            for (int col = 0; col < 64; ++col) {
+                if (m < D) part[col * D + m] = v[col];       // dW1[j][i]
+                else if (m == D) part[P1 + col] = v[col];    // db1[j]
             }
-        }
+        } else {
 #pragma unroll
-        for (int o = 0; o < 16; ++o) {
-            if (o >= c) continue;
-            if (m == D) part[o3 + HID * c + o] = v[128 + o];                // db3[o]
-            else if (m >= 64) part[o3 + o * HID + (m - 64)] = v[128 + o];   // dW3[o][i]
+            for (int col = 0; col < 64; ++col) {
+                if (m == D) part[o2 + HID * HID + col] = v[col];            // db2[j]
+                else if (m >= 64) part[o2 + col * HID + (m - 64)] = v[col];  // dW2[j][i]
+            }
+#pragma unroll
+            for (int o = 0; o < 16; ++o) {
+                if (o >= c) continue;
+                if (m == D) part[o3 + HID * c + o] = v[64 + o];                // db3[o]
+                else if (m >= 64) part[o3 + o * HID + (m - 64)] = v[64 + o];   // dW3[o][i]
+            }
         }
     }
     {
         float v = loss_acc;
 #pragma unroll
-        for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
-        if (lane == 0) atomicAdd(&s_loss[wg], v);
+        for (int sft = 16; sft > 0; sft >>= 1) v += __shfl_xor_sync(0xffffffffu, v, sft);
+        if (lane == 0 && h == 1) atomicAdd(&s_loss[slot], v);
     }
     tc_fence_before();
     __syncthreads();
@@ -1260,7 +1273,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         auto* k = d->activation == 1 ? train_kernel<8, 12, 1> : train_kernel<8, 12, 0>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TrainSmem::BYTES);
         if (e == cudaSuccess) {
-            k<<<grid, TRAIN_WG * 128, TrainSmem::BYTES, st>>>(tp);
+            k<<<grid, TRAIN_WG * 256, TrainSmem::BYTES, st>>>(tp);
             // t6: deterministic cross-CTA reduction, scaled by 1/(B c)
             reduce_kernel<<<(int)((P + 31) / 32), 256, 0, st>>>(t->partial, (size_t)P, t->loss_partial,
                                                                  grid, (int)P, tp.inv_bc, buf->grad_par, loss, status);
