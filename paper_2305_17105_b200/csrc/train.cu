@@ -221,8 +221,8 @@ template <int C0, int C1, int ACT>
 __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_constant__ TrainParams p) {
     // Two independent tile pipelines ("slots") per CTA, 8 warps each.  The 4 TMEM lane
     // quarters of a 128-texel tile are served by two warps each that split the columns: half
-    // h = 0 owns columns [0, 32) of every 64-wide activation (and the G0 part of X / dX), half
-    // h = 1 columns [32, 64) (and the G1 / PE / LOD part, the reference texels, the loss).
+    // h = 0 owns columns [0, 32) of every 64-wide activation (and the G0 part of X / dX, the
+    // reference texels and the loss), half h = 1 columns [32, 64) (and the G1 / PE / LOD part).
     using S = TrainSmem;
     constexpr int D = 4 * C0 + C1 + 13;
     constexpr int NLAT = 4 * C0 + C1;   // latent columns of X
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
     struct Fetch {
         Texel t;
         uint32_t v[24];    // h = 0: G0 taps (4 x uint4); h = 1: G1 taps (4 x 3 x uint2)
-        uint32_t ref[8];   // h = 1: reference channels (fp16 pairs)
+        uint32_t ref[8];   // h = 0: reference channels (fp16 pairs)
     };
     auto fetch = [&](int tile, Fetch& f) {
         f.t = texel_of(tile);
@@ -361,6 +361,14 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
                 f.v[4 * t + 2] = v.z;
                 f.v[4 * t + 3] = v.w;
             }
+            const uint16_t* rp = p.ref + (int64_t)f.t.y * p.ref_stride + (int64_t)f.t.x * c;
+#pragma unroll
+            for (int o = 0; o < 8; ++o) {
+                uint16_t lo = 0, hi = 0;
+                if (2 * o < c) lo = __ldg(rp + 2 * o);
+                if (2 * o + 1 < c) hi = __ldg(rp + 2 * o + 1);
+                f.ref[o] = (uint32_t)lo | ((uint32_t)hi << 16);
+            }
         } else {
             int tx[2], ty[2];
             uint32_t ax, ay;
@@ -375,14 +383,6 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
                     f.v[6 * t + 2 * e] = v.x;
                     f.v[6 * t + 2 * e + 1] = v.y;
                 }
-            }
-            const uint16_t* rp = p.ref + (int64_t)f.t.y * p.ref_stride + (int64_t)f.t.x * c;
-#pragma unroll
-            for (int o = 0; o < 8; ++o) {
-                uint16_t lo = 0, hi = 0;
-                if (2 * o < c) lo = __ldg(rp + 2 * o);
-                if (2 * o + 1 < c) hi = __ldg(rp + 2 * o + 1);
-                f.ref[o] = (uint32_t)lo | ((uint32_t)hi << 16);
             }
         }
     };
@@ -499,9 +499,9 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
             mma_commit(bar);
         }
         wait_mma();
-        // ---- t4: mean-L2 loss (R17) on half 1 (it holds the reference); delta3 = 2 (y - R)
+        // ---- t4: mean-L2 loss (R17) on half 0 (it holds the reference); delta3 = 2 (y - R)
         // fed unscaled, 1/(B c) applied in fp32
-        if (h == 1) {
+        if (h == 0) {
             uint32_t r[16];
             tmem_ld16(t_s + lane_off, r);
             tmem_wait_ld();
@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
         float v = loss_acc;
 #pragma unroll
         for (int sft = 16; sft > 0; sft >>= 1) v += __shfl_xor_sync(0xffffffffu, v, sft);
-        if (lane == 0 && h == 1) atomicAdd(&s_loss[slot], v);
+        if (lane == 0 && h == 0) atomicAdd(&s_loss[slot], v);
     }
     tc_fence_before();
     __syncthreads();
