@@ -183,7 +183,7 @@ def run_ours(args, rank, world, local_rank):
             return
         batch = ntc.make_batch(0, crop_sets[i], train["ref"], W * C)
         ntc.ntc_train_step(train["tr"], train["buf"], batch, hp, train["loss"], train["status"])
-        launches["train"] += 4  # prep (+ weight image), fused forward/backward, reduce, adam
+        launches["train"] += 3  # prep (+ weight image), fused forward/backward, reduce + Adam
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 

@@ -769,54 +769,73 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
     if (warp == 0) tmem_dealloc(*s_tmem, 512);
 }
 
-// fixed-order reduction of the per-CTA partials (deterministic), scaled by 1/(B c): block =
-// 32 parameters x 8 partial groups; group g owns partials g, g+8, ... and issues all of its
-// (<= RED_MAXK) loads before summing them in order; the 8 group sums are then added in
-// order.  Block 0 also reduces the loss partials with a fixed-shape tree.
 constexpr int RED_MAXK = 32;  // nparts <= 8 * RED_MAXK (grid <= 256 CTAs)
-__global__ void __launch_bounds__(256) reduce_kernel(const float* __restrict__ partial, size_t part_stride,
-                                                     const float* __restrict__ loss_partial, int nparts, int P,
-                                                     float inv_bc, float* __restrict__ grad, float* __restrict__ loss,
-                                                     int32_t* __restrict__ status) {
+struct ReduceArgs {
+    const float* partial;
+    size_t part_stride;
+    const float* loss_partial;
+    int nparts, P;
+    float inv_bc;
+    float* grad;
+    float* loss;
+    int32_t* status;
+};
+
+// one block: 32 parameters x 8 partial groups (blockIdx `blk`); returns the reduced, scaled
+// gradient of parameter `i` on the group-0 threads (undefined elsewhere)
+__device__ __forceinline__ float reduce_block(const ReduceArgs& r, int blk, int& i_out) {
     __shared__ float s[8][33];
     __shared__ float sl[256];
     const int px = threadIdx.x & 31, g = threadIdx.x >> 5;
-    const int i = blockIdx.x * 32 + px;
+    const int i = blk * 32 + px;
     float v[RED_MAXK];
 #pragma unroll
     for (int k = 0; k < RED_MAXK; ++k) {
         const int w = g + 8 * k;
-        v[k] = (i < P && w < nparts) ? __ldg(partial + (size_t)w * part_stride + i) : 0.0f;
+        v[k] = (i < r.P && w < r.nparts) ? __ldg(r.partial + (size_t)w * r.part_stride + i) : 0.0f;
     }
     float t = 0.0f;
 #pragma unroll
     for (int k = 0; k < RED_MAXK; ++k) t += v[k];
     s[g][px] = t;
-    if (blockIdx.x == 0) {
-        const int nl = nparts * TRAIN_WG;  // <= 2 * 256
+    if (blk == 0) {
+        const int nl = r.nparts * TRAIN_WG;  // <= 2 * 256
         float l = 0.0f;
-        if ((int)threadIdx.x < nl) l = loss_partial[threadIdx.x];
-        if ((int)threadIdx.x + 256 < nl) l += loss_partial[threadIdx.x + 256];
+        if ((int)threadIdx.x < nl) l = r.loss_partial[threadIdx.x];
+        if ((int)threadIdx.x + 256 < nl) l += r.loss_partial[threadIdx.x + 256];
         sl[threadIdx.x] = l;
     }
     __syncthreads();
-    if (g == 0 && i < P) {
+    float gr = 0.0f;
+    if (g == 0 && i < r.P) {
         float u = 0.0f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) u += s[k][px];
-        grad[i] = u * inv_bc;
+        gr = u * r.inv_bc;
+        r.grad[i] = gr;
     }
-    if (blockIdx.x == 0) {
-        for (int h = 128; h > 0; h >>= 1) {
-            if ((int)threadIdx.x < h) sl[threadIdx.x] += sl[threadIdx.x + h];
+    if (blk == 0) {
+        for (int hh = 128; hh > 0; hh >>= 1) {
+            if ((int)threadIdx.x < hh) sl[threadIdx.x] += sl[threadIdx.x + hh];
             __syncthreads();
         }
         if (threadIdx.x == 0) {
-            const float l = sl[0] * inv_bc;
-            *loss = l;
-            if (!isfinite(l) && status) atomicOr(status, (int)NTC_ERR_NONFINITE);
+            const float l = sl[0] * r.inv_bc;
+            *r.loss = l;
+            if (!isfinite(l) && r.status) atomicOr(r.status, (int)NTC_ERR_NONFINITE);
         }
     }
+    i_out = (g == 0 && i < r.P) ? i : -1;
+    return gr;
+}
+
+// fixed-order reduction of the per-CTA partials (deterministic), scaled by 1/(B c): block =
+// 32 parameters x 8 partial groups; group g owns partials g, g+8, ... and issues all of its
+// (<= RED_MAXK) loads before summing them in order; the 8 group sums are then added in
+// order.  Block 0 also reduces the loss partials with a fixed-shape tree.
+__global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ ReduceArgs r) {
+    int i;
+    reduce_block(r, blockIdx.x, i);
 }
 
 // ------------------------------------------------------------------ t8: Adam + clamp
@@ -849,17 +868,40 @@ __device__ __forceinline__ void adam_one(float& p, float& m, float& v, float g, 
     p -= lr * (m / a.c1) / (sqrtf(v / a.c2) + a.eps);
 }
 
+__device__ __forceinline__ void adam_weight(const AdamParams& a, int64_t i, float g) {
+    float p = a.params[i], m = a.m_par[i], v = a.v_par[i];
+    adam_one(p, m, v, g, a.lr_w, a);
+    a.params[i] = p;
+    a.m_par[i] = m;
+    a.v_par[i] = v;
+}
+
+__device__ void adam_latent(const AdamParams& a, int64_t j);
+
 __global__ void adam_kernel(const __grid_constant__ AdamParams a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < a.P) {  // weights: dense
-        float p = a.params[i], m = a.m_par[i], v = a.v_par[i];
-        adam_one(p, m, v, a.grad_par[i], a.lr_w, a);
-        a.params[i] = p;
-        a.m_par[i] = m;
-        a.v_par[i] = v;
+        adam_weight(a, i, a.grad_par[i]);
         return;
     }
-    const int64_t j = i - a.P;
+    adam_latent(a, i - a.P);
+}
+
+// GRADS|APPLY in one launch after the fused forward/backward: blocks [0, rblocks) reduce the
+// weight-gradient partials and apply Adam to the weights they just reduced; the remaining
+// blocks apply Adam to the footprint latents (their gradients are complete).
+__global__ void __launch_bounds__(256) reduce_adam_kernel(const __grid_constant__ ReduceArgs r,
+                                                          const __grid_constant__ AdamParams a, int rblocks) {
+    if ((int)blockIdx.x < rblocks) {
+        int i;
+        const float g = reduce_block(r, blockIdx.x, i);
+        if (i >= 0) adam_weight(a, i, g);
+        return;
+    }
+    adam_latent(a, (int64_t)(blockIdx.x - rblocks) * blockDim.x + threadIdx.x);
+}
+
+__device__ void adam_latent(const AdamParams& a, int64_t j) {
     if (a.freeze) return;
     int64_t li;
     int bits;
@@ -1170,6 +1212,9 @@ extern "C" ntc_status ntc_boxes_copy(const ntc_desc* d, const int32_t* boxes, in
 
 static ntc_status apply_step(const ntc_desc* d, const ntc_train_buffers* buf, const std::vector<Box>& boxes,
                              const ntc_train_hparams* hp, cudaStream_t st);
+static int64_t build_adam(const ntc_desc* d, const ntc_train_buffers* buf, const std::vector<Box>& boxes,
+                          const ntc_train_hparams* hp, AdamParams& a);
+static bool apply_buffers_ok(const ntc_train_buffers* buf);
 
 extern "C" ntc_status ntc_train_apply_boxes(ntc_trainer* t, const ntc_desc* d, const ntc_train_buffers* buf,
                                             const int32_t* boxes, int32_t n, const ntc_train_hparams* hp,
@@ -1274,9 +1319,20 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TrainSmem::BYTES);
         if (e == cudaSuccess) {
             k<<<grid, TRAIN_WG * 256, TrainSmem::BYTES, st>>>(tp);
-            // t6: deterministic cross-CTA reduction, scaled by 1/(B c)
-            reduce_kernel<<<(int)((P + 31) / 32), 256, 0, st>>>(t->partial, (size_t)P, t->loss_partial,
-                                                                 grid, (int)P, tp.inv_bc, buf->grad_par, loss, status);
+            // t6: deterministic cross-CTA reduction, scaled by 1/(B c); with APPLY in the same
+            // call, t8 rides in the same launch (weights Adam'd as they are reduced)
+            const ReduceArgs ra{t->partial, (size_t)P, t->loss_partial, grid, (int)P, tp.inv_bc, buf->grad_par, loss,
+                                status};
+            const int rblocks = (int)((P + 31) / 32);
+            if ((flags & NTC_STEP_APPLY) && apply_buffers_ok(buf)) {
+                AdamParams a;
+                const int64_t nlat = build_adam(d, buf, boxes, hp, a);
+                reduce_adam_kernel<<<rblocks + (int)((nlat + 255) / 256), 256, 0, st>>>(ra, a, rblocks);
+                e = cudaGetLastError();
+                if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
+                return NTC_OK;
+            }
+            reduce_kernel<<<rblocks, 256, 0, st>>>(ra);
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
@@ -1285,16 +1341,11 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
     return NTC_OK;
 }
 
-// t8: Adam on the weights (dense) and on the latents of `boxes` (footprint-sparse unless
-// dense_latent_adam), then the latent clamp
-static ntc_status apply_step(const ntc_desc* d, const ntc_train_buffers* buf, const std::vector<Box>& boxes,
-                             const ntc_train_hparams* hp, cudaStream_t st) {
+// t8 parameters: Adam on the weights (dense) and on the latents of `boxes` (footprint-sparse
+// unless dense_latent_adam), then the latent clamp.  Returns the latent work-item count.
+static int64_t build_adam(const ntc_desc* d, const ntc_train_buffers* buf, const std::vector<Box>& boxes,
+                          const ntc_train_hparams* hp, AdamParams& a) {
     const int64_t P = ntc_num_params(d), NL = ntc_num_latents(d);
-    cudaError_t e = cudaSuccess;
-    if (!buf->latents || !buf->m_lat || !buf->v_lat || !buf->grad_lat || !buf->params || !buf->m_par ||
-        !buf->v_par || !buf->grad_par)
-        return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
-    AdamParams a;
     memset(&a, 0, sizeof a);
     a.nbox = (int32_t)boxes.size();
     const int32_t n = box_prefix(boxes, a.box, a.box_start);
@@ -1331,9 +1382,20 @@ static ntc_status apply_step(const ntc_desc* d, const ntc_train_buffers* buf, co
         acc = o1 + (int64_t)r1 * r1 * d->c1;
     }
     a.grid_start[2 * L] = acc;
-    const int64_t total = P + (hp->freeze_latents ? 0 : (hp->dense_latent_adam ? NL : (int64_t)n));
+    return hp->freeze_latents ? 0 : (hp->dense_latent_adam ? NL : (int64_t)n);
+}
+
+static bool apply_buffers_ok(const ntc_train_buffers* buf) {
+    return buf->latents && buf->m_lat && buf->v_lat && buf->grad_lat && buf->params && buf->m_par && buf->v_par &&
+           buf->grad_par;
+}
+
+static ntc_status apply_step(const ntc_desc* d, const ntc_train_buffers* buf, const std::vector<Box>& boxes,
+                             const ntc_train_hparams* hp, cudaStream_t st) {
+    if (!apply_buffers_ok(buf)) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+    AdamParams a;
+    const int64_t total = ntc_num_params(d) + build_adam(d, buf, boxes, hp, a);
     adam_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
-    return NTC_OK;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? NTC_OK : api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
 }

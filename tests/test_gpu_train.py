@@ -233,3 +233,32 @@ def test_nonfinite_loss_sets_status(O):
                        flags=ntc.NTC_STEP_GRADS)
     torch.cuda.synchronize()
     assert st.item() & ntc.NTC_ERR_NONFINITE
+
+
+def test_fused_grads_apply_equals_split_calls(O):
+    """GRADS|APPLY in one call (reduction and Adam share a launch) equals a GRADS call followed
+    by an APPLY call: bit-identical weights and weight moments (the weight-gradient reduction
+    is deterministic); the latents to fp32 rounding (the latent-gradient scatter uses float
+    atomics, whose summation order varies between runs)."""
+    d, lat, par, ref, crops = _setup(O, 128, 9, 77, 0, 3, 40)
+    refd = torch.from_numpy(ref.view(np.int16)).to(DEV)
+    out = []
+    for split in (False, True):
+        tr = ntc.Trainer(d)
+        t = _gpu_buffers(O, d, lat, par)
+        bufs = ntc.make_buffers(t)
+        for step in (1, 2):
+            hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, step, 5, 1, 0)
+            batch = ntc.make_batch(0, gen_crops(300 + step, 128, 0, 3, 40), refd, 128 * 9)
+            loss = torch.zeros(1, device=DEV)
+            if split:
+                ntc.ntc_train_step(tr, bufs, batch, hp, loss, flags=ntc.NTC_STEP_GRADS)
+                ntc.ntc_train_step(tr, bufs, batch, hp, loss, flags=ntc.NTC_STEP_APPLY)
+            else:
+                ntc.ntc_train_step(tr, bufs, batch, hp, loss)
+        torch.cuda.synchronize()
+        out.append({k: t[k].cpu().numpy().copy() for k in ("params", "m_par", "v_par", "latents", "m_lat", "v_lat")})
+    for k in ("params", "m_par", "v_par"):
+        assert np.array_equal(out[0][k], out[1][k]), k
+    for k in ("latents", "m_lat", "v_lat"):
+        assert np.allclose(out[0][k], out[1][k], rtol=1e-4, atol=1e-9), k
