@@ -76,16 +76,22 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, i
     }
 }
 
+#ifndef DECODE_NWG
+#define DECODE_NWG 4
+#endif
 template <class P, int HM>
 struct DecodeSmem {
-    static constexpr int NWG = P::K1_ATOMS == 1 ? 4 : 2;  // warpgroups per CTA
+    // warpgroups per CTA x tile contexts per warpgroup (8 contexts x 64 TMEM columns = 512
+    // for K1 = 64; the K1 > 64 profiles' 32 KB A tiles leave SMEM for 4 contexts)
+    static constexpr int NWG = P::K1_ATOMS == 1 ? DECODE_NWG : 2;
+    static constexpr int NC = P::K1_ATOMS == 1 ? 8 / DECODE_NWG : 2;
     static constexpr uint32_t W1_BYTES = P::K1_ATOMS * 64 * 128;
     static constexpr uint32_t W2_BYTES = 2 * 64 * 128;  // weights atom + bias atom
     static constexpr uint32_t W3_BYTES = 2 * 16 * 128;
     static constexpr uint32_t WIMG = W1_BYTES + HM * W2_BYTES + W3_BYTES;
     static constexpr uint32_t ONES = 128 * 128;         // constant A tile: column 0 = 1
     static constexpr uint32_t ABUF = P::K1_ATOMS * 128 * 128;  // one per tile context
-    static constexpr uint32_t BYTES = 1024 + WIMG + ONES + NWG * 2 * ABUF + 128 /*pe*/ + 128 /*bars*/ + 16;
+    static constexpr uint32_t BYTES = 1024 + WIMG + ONES + NWG * NC * ABUF + 128 /*pe*/ + 128 /*bars*/ + 16;
 };
 
 // The tile range a CTA is working through, with the material it belongs to (uniform).
@@ -185,15 +191,15 @@ struct Ctx {
 template <class P, int HM, bool MULTI, int ACT>
 __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTable* mt) {
     using S = DecodeSmem<P, HM>;
-    constexpr int NW = S::NWG;
+    constexpr int NW = S::NWG, NC = S::NC;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* s_w = smem;
     uint8_t* s_ones = smem + S::WIMG;
     uint8_t* s_a = s_ones + S::ONES;
-    uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_a + NW * 2 * S::ABUF);
+    uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_a + NW * NC * S::ABUF);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_pe + 32);
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * NW);
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + NC * NW);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wg = warp >> 2, q = warp & 3, row = q * 32 + lane;
@@ -207,7 +213,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     }
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
     if (tid == 0) {
-        for (int i = 0; i < 2 * NW; ++i) mbar_init(&s_bar[i], 1);
+        for (int i = 0; i < NC * NW; ++i) mbar_init(&s_bar[i], 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -232,32 +238,32 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     // spread over the four SM sub-partitions instead of piling up on warp 0's.
     auto handoff = [&](const Ctx<P>& C) {
         if (q == C.iq)
-            named_bar_sync(1 + wg * 2 + C.id, 128);
+            named_bar_sync(1 + wg * NC + C.id, 128);
         else
-            named_bar_arrive(1 + wg * 2 + C.id, 128);
+            named_bar_arrive(1 + wg * NC + C.id, 128);
     };
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
     // single material: tiles blockIdx-strided over [first, ntiles); multi: per-run ranges
     int ntiles = p.mode == 0 ? p.n_tiles : (int)((p.nq + TILE_M - 1) / TILE_M);
-    int stride = (int)gridDim.x * NW * 2;  // tiles advance by 2 contexts per warpgroup
+    int stride = (int)gridDim.x * NW * NC;  // tiles advance by NC contexts per warpgroup
     Run R;
     R.grids = nullptr;
     R.b3 = nullptr;
     R.perm = MULTI ? mt->perm : nullptr;
     R.ts0 = R.seg0 = R.cnt = 0;
 
-    Ctx<P> cx[2];
+    Ctx<P> cx[NC];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < NC; ++c) {
         cx[c].phase = 0;
-        cx[c].abuf = smem_u32(s_a + (wg * 2 + c) * S::ABUF);
-        cx[c].tcol = tmem + (uint32_t)(wg * 128 + c * 64);
-        cx[c].bar = &s_bar[wg * 2 + c];
+        cx[c].abuf = smem_u32(s_a + (wg * NC + c) * S::ABUF);
+        cx[c].tcol = tmem + (uint32_t)((wg * NC + c) * 64);
+        cx[c].bar = &s_bar[wg * NC + c];
         cx[c].id = c;
-        cx[c].iq = (wg * 2 + c) & 3;
+        cx[c].iq = (wg * NC + c) & 3;
         cx[c].adesc = umma_desc_k_sw128(cx[c].abuf);
         if (!MULTI) {
-            cx[c].tile = (p.mode == 0 ? p.tile_first : 0) + ((int)blockIdx.x * NW + wg) * 2 + c;
+            cx[c].tile = (p.mode == 0 ? p.tile_first : 0) + ((int)blockIdx.x * NW + wg) * NC + c;
             if (cx[c].tile < ntiles) fetch_tile<P, MULTI>(p, R, cx[c].tile, row, cx[c].nxt);
         }
     }
@@ -335,21 +341,27 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     auto run = [&](int first) {
         if (MULTI) {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                cx[c].tile = first + wg * 2 + c;
+            for (int c = 0; c < NC; ++c) {
+                cx[c].tile = first + wg * NC + c;
                 if (cx[c].tile < ntiles) fetch_tile<P, MULTI>(p, R, cx[c].tile, row, cx[c].nxt);
             }
         }
-        phase0(cx[0]);
-        phase0(cx[1]);
-        while (cx[0].tile < ntiles || cx[1].tile < ntiles) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) phase0(cx[c]);
+        auto busy = [&]() {
+            bool b = false;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) b = b || cx[c].tile < ntiles;
+            return b;
+        };
+        while (busy()) {
 #pragma unroll
             for (int layer = 0; layer <= HM; ++layer) {
-                phase_hidden(cx[0], layer);
-                phase_hidden(cx[1], layer);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) phase_hidden(cx[c], layer);
             }
-            phase_out(cx[0]);
-            phase_out(cx[1]);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) phase_out(cx[c]);
         }
     };
     if constexpr (!MULTI) {
@@ -375,7 +387,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
             R.seg0 = __ldg(mt->seg + m);
             R.cnt = __ldg(mt->seg + m + 1) - R.seg0;
             ntiles = e;
-            stride = NW * 2;
+            stride = NW * NC;
             run(pos);
             pos = e;
         }
