@@ -162,6 +162,83 @@ __device__ __forceinline__ void fetch_texel(const DecodeParams& p, const uint8_t
     }
 }
 
+// ------------------------------------------------------------------ assembly pieces
+// G0 of NTC 0.2 (C0 = 8, B0 = 2): 16 words from the four 16-bit tap cells
+__device__ __forceinline__ void g0_words_c8b2(const uint32_t (&cell)[4], uint32_t (&w)[16]) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const uint32_t y = __byte_perm(cell[t], 0u, 0x4140);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[4 * t + k] = dequant2<2>((y >> (2 * k)) & 0x00030003u);
+    }
+}
+
+// G1: bilinear as integer multiply-adds on two 16-bit lanes:
+// S = sum_t wt_t * code_t (< 2^16), value = (S - 256 (N/2-1)) / (256 N), exact in fp32,
+// rounded once to fp16.  cell[t][wd]: 32-bit word wd of tap t's packed cell.
+template <class P, int NWD>
+__device__ __forceinline__ void g1_words(const uint32_t (&cell)[4][NWD], const uint32_t (&wt)[4],
+                                         uint32_t (&out)[P::C1 / 2]) {
+    static_assert(P::B1 == 4, "G1 path assumes 4-bit codes (all Table 2 profiles)");
+    constexpr int NL = P::C1 / 2;
+    uint32_t S[NL];
+    float v[P::C1];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        uint32_t l[NL];
+        int cb[NL];  // first channel of each lane pair, second = cb + step
+        int st[NL];
+        int n = 0;
+#pragma unroll
+        for (int wd = 0; wd * 8 < P::C1; ++wd) {
+            const int nch = P::C1 - wd * 8 >= 8 ? 8 : P::C1 - wd * 8;
+            if (nch == 8) {
+                nib_lanes<8>(cell[t][wd], l + n);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 4; }
+                n += 4;
+            } else if (nch == 4) {
+                nib_lanes<4>(cell[t][wd], l + n);
+#pragma unroll
+                for (int q = 0; q < 2; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 2; }
+                n += 2;
+            } else {
+                nib_lanes<2>(cell[t][wd], l + n);
+                cb[n] = wd * 8;
+                st[n] = 1;
+                n += 1;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NL; ++i) S[i] = t == 0 ? l[i] * wt[0] : S[i] + l[i] * wt[t];
+        if (t == 3) {
+            constexpr float SC = 1.0f / (256.0f * 16.0f);
+            constexpr float BI = -(8388608.0f + 256.0f * 7.0f) / (256.0f * 16.0f);
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                v[cb[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7610)), SC, BI);
+                v[cb[i] + st[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7632)), SC, BI);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < P::C1 / 2; ++k) out[k] = pack_half2(v[2 * k], v[2 * k + 1]);
+}
+
+// PE from the per-axis table, then LOD + bias one: 7 words
+__device__ __forceinline__ void pe_lod_words(const DecodeParams& p, const uint32_t* s_pe, int m, int x, int y,
+                                             uint32_t (&w)[7]) {
+    const uint4 px = *reinterpret_cast<const uint4*>(s_pe + 4 * (x & 7));
+    const uint4 py = *reinterpret_cast<const uint4*>(s_pe + 4 * (y & 7));
+    w[0] = px.x;
+    w[1] = px.y;
+    w[2] = px.z;
+    w[3] = py.x;
+    w[4] = py.y;
+    w[5] = py.z;
+    w[6] = p.lod_word[m];
+}
+
 // ------------------------------------------------------------------ assembly (a2-a4)
 // X = [G0 taps (permuted pairs) | bilinear G1 | PE_x(6) | PE_y(6) | LOD | 1 | 0 ...] as
 // K1W half2 words; the trailing 1 multiplies the b1 column of the W1 image.
@@ -170,12 +247,11 @@ __device__ __forceinline__ void assemble_words(const DecodeParams& p, const uint
                                                uint32_t (&w)[P::K1W]) {
     // ---- G0: four unfiltered taps (learned interpolation)
     if constexpr (P::C0 == 8 && P::B0 == 2) {
+        const uint32_t cell[4] = {f.g0[0].w[0], f.g0[1].w[0], f.g0[2].w[0], f.g0[3].w[0]};
+        uint32_t g[16];
+        g0_words_c8b2(cell, g);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const uint32_t y = __byte_perm(f.g0[t].w[0], 0u, 0x4140);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) w[4 * t + k] = dequant2<2>((y >> (2 * k)) & 0x00030003u);
-        }
+        for (int i = 0; i < 16; ++i) w[i] = g[i];
     } else if constexpr (P::C0 == 12 && P::B0 == 2) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -209,66 +285,26 @@ __device__ __forceinline__ void assemble_words(const DecodeParams& p, const uint
             for (int k = 0; k < 8; ++k) w[8 * t + k] = dequant2<4>(l[k]);
         }
     }
-    // ---- G1: bilinear as integer multiply-adds on two 16-bit lanes:
-    // S = sum_t wt_t * code_t (< 2^16), value = (S - 256 (N/2-1)) / (256 N), exact in fp32,
-    // rounded once to fp16.
-    static_assert(P::B1 == 4, "G1 path assumes 4-bit codes (all Table 2 profiles)");
+    // ---- G1 bilinear, PE, LOD
     {
-        constexpr int NL = P::C1 / 2;
-        uint32_t S[NL];
-        float v[P::C1];
+        constexpr int NWD = P::CELL1 >= 4 ? P::CELL1 / 4 : 1;
+        uint32_t cell[4][NWD];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            uint32_t l[NL];
-            int cb[NL];  // first channel of each lane pair, second = cb + step
-            int st[NL];
-            int n = 0;
+        for (int t = 0; t < 4; ++t)
 #pragma unroll
-            for (int wd = 0; wd * 8 < P::C1; ++wd) {
-                const int nch = P::C1 - wd * 8 >= 8 ? 8 : P::C1 - wd * 8;
-                if (nch == 8) {
-                    nib_lanes<8>(f.g1[t].w[wd], l + n);
+            for (int wd = 0; wd < NWD; ++wd) cell[t][wd] = f.g1[t].w[wd];
+        uint32_t g[P::C1 / 2];
+        g1_words<P, NWD>(cell, f.wt, g);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 4; }
-                    n += 4;
-                } else if (nch == 4) {
-                    nib_lanes<4>(f.g1[t].w[wd], l + n);
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 2; }
-                    n += 2;
-                } else {
-                    nib_lanes<2>(f.g1[t].w[wd], l + n);
-                    cb[n] = wd * 8;
-                    st[n] = 1;
-                    n += 1;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < NL; ++i) S[i] = t == 0 ? l[i] * f.wt[0] : S[i] + l[i] * f.wt[t];
-            if (t == 3) {
-                constexpr float SC = 1.0f / (256.0f * 16.0f);
-                constexpr float BI = -(8388608.0f + 256.0f * 7.0f) / (256.0f * 16.0f);
-#pragma unroll
-                for (int i = 0; i < NL; ++i) {
-                    v[cb[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7610)), SC, BI);
-                    v[cb[i] + st[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7632)), SC, BI);
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < P::C1 / 2; ++k) w[2 * P::C0 + k] = pack_half2(v[2 * k], v[2 * k + 1]);
+        for (int k = 0; k < P::C1 / 2; ++k) w[2 * P::C0 + k] = g[k];
     }
-    // ---- PE from the per-axis table, then LOD + bias one
     constexpr int PEW = (4 * P::C0 + P::C1) / 2;
-    const uint4 px = *reinterpret_cast<const uint4*>(s_pe + 4 * (f.x & 7));
-    const uint4 py = *reinterpret_cast<const uint4*>(s_pe + 4 * (f.y & 7));
-    w[PEW + 0] = px.x;
-    w[PEW + 1] = px.y;
-    w[PEW + 2] = px.z;
-    w[PEW + 3] = py.x;
-    w[PEW + 4] = py.y;
-    w[PEW + 5] = py.z;
-    w[PEW + 6] = p.lod_word[f.m];
+    {
+        uint32_t pw[7];
+        pe_lod_words(p, s_pe, f.m, f.x, f.y, pw);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) w[PEW + k] = pw[k];
+    }
 #pragma unroll
     for (int k = PEW + 7; k < P::K1W; ++k) w[k] = 0u;
 }
