@@ -137,9 +137,19 @@ def _stream(stream=None):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+_DESC_CACHE = {}
+
+
 def make_desc(p) -> Desc:
-    """From any object with the ntc_desc field names (e.g. synth.Profile)."""
-    return Desc(*[int(getattr(p, f)) for f, _ in Desc._fields_])
+    """From any object with the ntc_desc field names (e.g. synth.Profile); cached per value
+    (the hot-path wrappers are called every training step)."""
+    if isinstance(p, Desc):
+        return p
+    key = tuple(int(getattr(p, f)) for f, _ in Desc._fields_)
+    d = _DESC_CACHE.get(key)
+    if d is None:
+        d = _DESC_CACHE[key] = Desc(*key)
+    return d
 
 
 # ---------------------------------------------------------------- geometry (host)

@@ -231,6 +231,9 @@ class StepPlan:
         self.recv_sizes = [size(b) for b in self.recv_boxes]
         self.send_all = _concat_boxes(self.send_boxes)
         self.recv_all = _concat_boxes(self.recv_boxes)
+        # identical on every rank (derived from the global plan): skip the two all-to-alls
+        # collectively when no rank reads outside its band (stratified crops usually do not)
+        self.any_halo = any(plan[a][b].size for a in range(world) for b in range(world))
 
 
 def _concat_boxes(lst):
@@ -314,9 +317,10 @@ class ShardedDataParallelTrainer:
         ns, nr = sum(pl.send_sizes), sum(pl.recv_sizes)
         sbuf, rbuf = self._buffers(ns, nr)
         # 1. halo latents from their owners (one batched pack, one all-to-all, one unpack)
-        self._copy(pl.send_all, self.t["latents"], sbuf, NTC_BOX_PACK)
-        self._exchange(sbuf, pl.send_sizes, rbuf, pl.recv_sizes)
-        self._copy(pl.recv_all, rbuf, self.t["latents"], NTC_BOX_UNPACK)
+        if pl.any_halo:
+            self._copy(pl.send_all, self.t["latents"], sbuf, NTC_BOX_PACK)
+            self._exchange(sbuf, pl.send_sizes, rbuf, pl.recv_sizes)
+            self._copy(pl.recv_all, rbuf, self.t["latents"], NTC_BOX_UNPACK)
         # 2. zero this rank's share of the global footprint, then GRADS on its own crops
         self._copy(pl.mine_g, None, self.t["grad_lat"], NTC_BOX_ZERO)
         loss = self.flat[self.P: self.P + 1]
@@ -327,9 +331,10 @@ class ShardedDataParallelTrainer:
         else:
             self.flat.zero_()
         # 3. halo gradients back to their owners (the reverse exchange), added there
-        self._copy(pl.recv_all, self.t["grad_lat"], rbuf, NTC_BOX_PACK)
-        self._exchange(rbuf, pl.recv_sizes, sbuf, pl.send_sizes)
-        self._copy(pl.send_all, sbuf, self.t["grad_lat"], NTC_BOX_ADD)
+        if pl.any_halo:
+            self._copy(pl.recv_all, self.t["grad_lat"], rbuf, NTC_BOX_PACK)
+            self._exchange(rbuf, pl.recv_sizes, sbuf, pl.send_sizes)
+            self._copy(pl.send_all, sbuf, self.t["grad_lat"], NTC_BOX_ADD)
         # 4. [dW | loss] all-reduce; 5. owners apply Adam to their band of the global footprint
         self.dist.all_reduce(self.flat, group=self.group)
         ntc_train_apply_boxes(self.trainer, self.bufs, pl.mine_g, hp)
