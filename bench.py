@@ -49,6 +49,15 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def _ncu_metric(kernel, name):
+    """One metric value of `kernel` in the committed ncu summary (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return float(json.load(f)["kernels"][kernel]["metrics"][name][0])
+    except Exception:
+        return None
+
+
 def _ncu_traffic(kernel):
     """dram read+write bytes per launch of `kernel` from the committed ncu summary (or None)."""
     try:
@@ -240,7 +249,16 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(achieved / peak_tf, 4), "traffic": tr_bytes,
                      "peak_source": f"{pk_src} bf16 dense burst (fp16 same rate)",
-                     "kernel": "ntc::decode_kernel", "flops_per_texel": decode_flops_per_texel(d)},
+                     "kernel": "ntc::decode_kernel", "flops_per_texel": decode_flops_per_texel(d),
+                     # SURVEY 8(d) diagnostics: HBM use of the same launch (live time, committed ncu
+                     # bytes) and the issue-slot utilisation that bounds the kernel (ncu)
+                     "diagnostics": {
+                         "dram_gbs": None if tr_bytes is None else round(tr_bytes / (dec / args.steps) / 1e9, 1),
+                         "dram_frac": None if tr_bytes is None else
+                         round(tr_bytes / (dec / args.steps) / 1e9 / pk["hbm_gbs"], 4),
+                         "issue_active_pct": _ncu_metric("decode", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                         "tensor_pipe_pct": _ncu_metric(
+                             "decode", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")}},
         "gpu_launches": args.steps + launches["train"],
         "clocks": clk.report(),
     })
@@ -253,7 +271,14 @@ def run_ours(args, rank, world, local_rank):
                         "NCCL all-to-all of halo latents and halo gradients, all-reduce of [dW | loss]",
                         "unit": "texel/s", "ms_per_step": trn / args.steps * 1e3, "workload": TRAIN_WORKLOAD,
                         "roofline": {"bound": "tensor", "achieved": round(tflops, 2), "peak": peak_tf,
-                                     "unit": "TFLOP/s", "frac": round(tflops / peak_tf, 4)}}
+                                     "unit": "TFLOP/s", "frac": round(tflops / peak_tf, 4),
+                                     "kernel": "ntc::train_kernel (+ prep, reduce/Adam in the step time)",
+                                     "flops_per_texel": train_flops_per_texel(d),
+                                     "diagnostics": {
+                                         "issue_active_pct": _ncu_metric(
+                                             "train", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                         "tensor_pipe_pct": _ncu_metric(
+                                             "train", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")}}}
     # e2e through the public API from pinned host buffers (rank 0 and every rank alike)
     res["e2e"] = e2e(args, ntc, torch, d, codes, wts, dev, world)
     if world == 1 and not args.no_extras:
