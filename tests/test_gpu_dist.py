@@ -176,3 +176,27 @@ def test_sharded_dp_matches_single_process():
         assert np.allclose(p, ref_par, rtol=1e-4, atol=1e-6)
         assert np.allclose(full, ref_lat, rtol=1e-4, atol=1e-6)
     assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
+
+
+def test_bench_two_ranks_json_line():
+    """bench.py's N > 1 path (torchrun, two ranks sharing cuda:0 over gloo): one JSON line
+    with the contract's keys, weak-scaling totals over both ranks, and the sharded
+    data-parallel training step."""
+    import json
+    import subprocess
+    import sys
+
+    env = dict(os.environ, NTC_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-extras"]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    r = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "dtype", "config", "roofline", "gpu_launches", "clocks", "e2e", "train"):
+        assert k in r, k
+    assert r["n_gpus"] == 2 and r["scaling"] == "weak" and r["value"] > 0
+    assert "sharded" in r["train"]["parallelism"]
