@@ -27,7 +27,6 @@
 namespace ntc {
 
 constexpr int MAX_BOXES = 256;
-constexpr int TRAIN_WG = 2;  // warpgroups (independent tile pipelines) per CTA
 
 struct Box {        // inclusive cell ranges of one grid
     int64_t off;    // element offset of the grid in the canonical latent array
@@ -54,8 +53,8 @@ struct TrainParams {
     const __half* noisy;
     float* grad_lat;
     const uint8_t* wimg;  // fp16 weight image (TrainSmem layout, WEND bytes)
-    float* partial;     // [grid * TRAIN_WG][P]
-    float* loss_partial;  // [grid * TRAIN_WG]
+    float* partial;     // [grid][P]
+    float* loss_partial;  // [grid * slots]
     int32_t P;
     int32_t debug_flags;  // profiling only (NTC_DEBUG_TRAIN env): 1 = skip the latent scatter
     int32_t freeze;       // frozen phase: no latent gradients
@@ -89,7 +88,7 @@ struct PrepParams {
     // fp16 weight image of the master weights, built by the trailing blocks of the same launch
     int32_t prep_blocks;  // blocks [0, prep_blocks) do t2; the rest build the image
     const float* params;
-    int32_t D, c;
+    int32_t D, c, hm;
     uint8_t* wimg;
 };
 
@@ -105,15 +104,26 @@ __device__ __forceinline__ void box_locate(const Box* box, const int32_t* start,
 }
 
 // ------------------------------------------------------------------ fused forward + backward
-struct TrainSmem {
-    // fp16 weight images (W1 with b1 at column D, W2, W3) + fp32 biases b2[64], b3[16]
-    static constexpr uint32_t W1 = 0, W2 = 8192, W3 = 16384, BIAS = 18432, WEND = 19456;
+// SMEM layout for depth HM (1: [D,64,64,c]; 2: [D,64,64,64,c], R11): fp16 weight images (W1 with
+// b1 at column D, W2, [W2b], W3 with 16 rows) + fp32 biases b2[64], [b2b[64]], b3[16]; then per
+// tile pipeline ("slot") the SW128 activation tiles.  Depth 2 needs 8 tiles per slot, which
+// leaves SMEM for one slot.
+template <int HM>
+struct TrainSmemT {
+    static constexpr uint32_t W1 = 0, W2 = 8192, W2B = 16384, W3 = 8192u * (1 + HM), BIAS = W3 + 2048;
+    static constexpr uint32_t NBIAS = 64 * HM + 16;
+    static constexpr uint32_t WEND = ((BIAS + 4 * NBIAS + 1023) / 1024) * 1024;
     static constexpr uint32_t TILE = 128 * 128;  // one 128 x 64 fp16 SW128 tile
-    enum { X = 0, H1 = 1, H2 = 2, G1 = 3, G2 = 4, D3 = 5, NT = 6 };
+    // G1 and G2 adjacent: [delta1 | delta2] is one N=128 operand of the weight-gradient MMA
+    // depth 1: X H1 H2 G1 G2 D3; depth 2: X H1 H2 H3 G1 G2 G3 D3
+    enum { X = 0, H1 = 1, H2 = 2, H3 = 3, G1 = 2 + HM, G2 = 3 + HM, G3 = 6, D3 = 3 + 2 * HM, NT = 4 + 2 * HM };
+    static constexpr int SLOTS = HM == 1 ? 2 : 1;
     static constexpr uint32_t WG_BYTES = NT * TILE;
     static constexpr uint32_t MISC = 256 + 16 * NTC_MAX_CROPS + 4 * (NTC_MAX_CROPS + 1) + 12;
-    static constexpr uint32_t BYTES = 1024 + WEND + TRAIN_WG * WG_BYTES + MISC;
+    static constexpr uint32_t BYTES = 1024 + WEND + SLOTS * WG_BYTES + MISC;
 };
+using TrainSmem = TrainSmemT<1>;
+constexpr uint32_t TRAIN_WEND_MAX = TrainSmemT<2>::WEND;
 
 __device__ __forceinline__ void sts_row_chunk(uint32_t tile, int row, int chunk, uint32_t a, uint32_t b, uint32_t c,
                                               uint32_t d) {
@@ -144,20 +154,27 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 __device__ __forceinline__ uint32_t h2u(float a, float b) { return pack_half2(a, b); }
 
 // fp16 SW128 weight image of the current fp32 master weights (t3): W1 (+ b1 at column D, it
-// multiplies X's constant 1), W2, W3 (16 rows); b2 and b3 as fp32 values of their fp16 rounding
-// (R14), added in the epilogues
-constexpr int WIMG_ITEMS = 3 * 4096 + HID + 16;
-__device__ __forceinline__ void train_wimg_item(int i, const float* __restrict__ w, int D, int c, uint8_t* __restrict__ img) {
-    using S = TrainSmem;
-    if (i >= WIMG_ITEMS) return;
-    const int P1 = D * HID;
-    if (i >= 3 * 4096) {
-        const int j = i - 3 * 4096;
-        if (j < HID)
-            reinterpret_cast<float*>(img + S::BIAS)[j] = __half2float(__float2half_rn(w[P1 + HID + HID * HID + j]));
-        else if (j < HID + 16)
-            reinterpret_cast<float*>(img + S::BIAS)[j] =
-                (j - HID) < c ? __half2float(__float2half_rn(w[P1 + 2 * HID + HID * HID + HID * c + (j - HID)])) : 0.0f;
+// multiplies X's constant 1), W2, [W2b], W3 (16 rows); the hidden and output biases as fp32
+// values of their fp16 rounding (R14), added in the epilogues.  ABI parameter order: W1, b1,
+// W2, b2, [W2b, b2b], W3, b3.
+__host__ __device__ constexpr int wimg_items(int hm) { return (2 + hm) * 4096 + 64 * hm + 16; }
+template <int HM>
+__device__ __forceinline__ void train_wimg_item_t(int i, const float* __restrict__ w, int D, int c,
+                                                  uint8_t* __restrict__ img) {
+    using S = TrainSmemT<HM>;
+    if (i >= wimg_items(HM)) return;
+    const int P1 = D * HID;                  // b1
+    const int o3 = P1 + HID + HM * (HID * HID + HID);  // W3
+    float* bias = reinterpret_cast<float*>(img + S::BIAS);
+    if (i >= (2 + HM) * 4096) {
+        const int j = i - (2 + HM) * 4096;
+        if (j < 64 * HM) {  // hidden biases b2 (, b2b)
+            const int l = j / 64, o = j % 64;
+            bias[j] = __half2float(__float2half_rn(w[P1 + HID + l * (HID * HID + HID) + HID * HID + o]));
+        } else {            // b3 (16 slots, c used)
+            const int o = j - 64 * HM;
+            bias[j] = o < c ? __half2float(__float2half_rn(w[o3 + HID * c + o])) : 0.0f;
+        }
         return;
     }
     const int part = i / 4096, e = i % 4096, r = e / 64, k = e % 64;
@@ -166,12 +183,12 @@ __device__ __forceinline__ void train_wimg_item(int i, const float* __restrict__
     if (part == 0) {
         v = k < D ? w[r * D + k] : (k == D ? w[P1 + r] : 0.0f);
         base = S::W1;
-    } else if (part == 1) {
-        v = w[P1 + HID + r * HID + k];
-        base = S::W2;
+    } else if (part <= HM) {  // hidden matrix part-1
+        v = w[P1 + HID + (part - 1) * (HID * HID + HID) + r * HID + k];
+        base = part == 1 ? S::W2 : S::W2B;
     } else {
         if (r >= 16) return;
-        v = r < c ? w[P1 + HID + HID * HID + HID + r * HID + k] : 0.0f;
+        v = r < c ? w[o3 + r * HID + k] : 0.0f;
         base = S::W3;
     }
     *reinterpret_cast<__half*>(img + base + sw128_offset(r, k)) = __float2half_rn(v);
@@ -180,7 +197,13 @@ __device__ __forceinline__ void train_wimg_item(int i, const float* __restrict__
 // t2: noisy = latent + U(-Q/2, Q/2) (one draw per latent per step), grad = 0, over the footprint
 __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
     if ((int)blockIdx.x >= p.prep_blocks) {
-        if (p.wimg) train_wimg_item(((int)blockIdx.x - p.prep_blocks) * blockDim.x + threadIdx.x, p.params, p.D, p.c, p.wimg);
+        const int i = ((int)blockIdx.x - p.prep_blocks) * blockDim.x + threadIdx.x;
+        if (p.wimg) {
+            if (p.hm == 2)
+                train_wimg_item_t<2>(i, p.params, p.D, p.c, p.wimg);
+            else
+                train_wimg_item_t<1>(i, p.params, p.D, p.c, p.wimg);
+        }
         return;
     }
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -217,20 +240,23 @@ __device__ __forceinline__ void act_and_grad(float z, float& h, float& g) {
     }
 }
 
-template <int C0, int C1, int ACT>
-__global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_constant__ TrainParams p) {
+template <int C0, int C1, int ACT, int HM>
+__global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(const __grid_constant__ TrainParams p) {
     // Two independent tile pipelines ("slots") per CTA, 8 warps each.  The 4 TMEM lane
     // quarters of a 128-texel tile are served by two warps each that split the columns: half
     // h = 0 owns columns [0, 32) of every 64-wide activation (and the G0 part of X / dX, the
     // reference texels and the loss), half h = 1 columns [32, 64) (and the G1 / PE / LOD part).
-    using S = TrainSmem;
+    // Depth HM = 2 ([D,64,64,64,c], R11) adds a hidden layer (H3/G3 tiles, one more forward
+    // and backward round trip, a third weight-gradient stack) and runs one slot per CTA.
+    using S = TrainSmemT<HM>;
+    constexpr int SLOTS = S::SLOTS;
     constexpr int D = 4 * C0 + C1 + 13;
     constexpr int NLAT = 4 * C0 + C1;   // latent columns of X
     static_assert(D < 64 && NLAT <= 48 && 4 * C0 == 32, "training kernel: K1 = 64, 32 G0 columns");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::WEND + TRAIN_WG * S::WG_BYTES);
-    float* s_loss = reinterpret_cast<float*>(s_bar + 2 * TRAIN_WG);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::WEND + SLOTS * S::WG_BYTES);
+    float* s_loss = reinterpret_cast<float*>(s_bar + 2 * SLOTS);
     uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_loss + 4);
     uint32_t* s_tmem = s_pe + 32;
     int4* s_crop = reinterpret_cast<int4*>(s_tmem + 4);
@@ -249,7 +275,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
     if (tid < NTC_MAX_CROPS) s_crop[tid] = make_int4(p.crop[tid][0], p.crop[tid][1], p.crop[tid][2], p.crop[tid][3]);
     if (tid <= NTC_MAX_CROPS) s_ts[tid] = p.tile_start[tid];
     if (tid == 0) {
-        for (int i = 0; i < 2 * TRAIN_WG; ++i) mbar_init(&s_bar[i], 1);
+        for (int i = 0; i < 2 * SLOTS; ++i) mbar_init(&s_bar[i], 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -261,17 +287,21 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
     __syncthreads();
     tc_fence_after();
 
-    // TMEM per slot: [0,128) dW-a accumulator, [128,144) dW-b, [192,256) scratch
-    const uint32_t tbase = *s_tmem + (uint32_t)slot * 256u;
-    const uint32_t t_acc_a = tbase, t_acc_b = tbase + 128, t_s = tbase + 192;
+    // TMEM per slot: depth 1: [0,128) dW-a accumulator, [128,144) dW-b, [192,256) scratch;
+    // depth 2: [0,128) dW-a, [128,192) dW-m (the middle layer), [192,208) dW-b, [256,320) scratch
+    const uint32_t tbase = *s_tmem + (uint32_t)slot * (512u / SLOTS);
+    const uint32_t t_acc_a = tbase, t_acc_m = tbase + 128, t_acc_b = tbase + (HM == 1 ? 128 : 192);
+    const uint32_t t_s = tbase + (HM == 1 ? 192 : 256);
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t sbase = smem_u32(smem);
     const uint32_t tiles = sbase + S::WEND + (uint32_t)slot * S::WG_BYTES;
     const uint32_t tX = tiles + S::X * S::TILE, tH1 = tiles + S::H1 * S::TILE, tH2 = tiles + S::H2 * S::TILE;
     const uint32_t tG1 = tiles + S::G1 * S::TILE, tG2 = tiles + S::G2 * S::TILE, tD3 = tiles + S::D3 * S::TILE;
+    const uint32_t tH3 = tiles + S::H3 * S::TILE, tG3 = tiles + S::G3 * S::TILE;  // depth 2 only
+    const uint32_t tHL = HM == 1 ? tH2 : tH3, tGL = HM == 1 ? tG2 : tG3;        // last hidden layer
     const bool issuer = (warp & 7) == slot * 2 && lane == 0;  // the two issuers on different sub-partitions
     uint64_t* bar = &s_bar[slot];
-    uint64_t* bar2 = &s_bar[TRAIN_WG + slot];
+    uint64_t* bar2 = &s_bar[SLOTS + slot];
     uint32_t phase = 0, phase2 = 0;
     bool pending_w = false;  // weight-gradient MMAs of the previous tile in flight
     auto sync_slot = [&]() {
@@ -285,15 +315,18 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
         tc_fence_after();
     };
     const uint64_t dW1 = umma_desc_k_sw128(sbase + S::W1), dW2 = umma_desc_k_sw128(sbase + S::W2);
-    const uint64_t dW3 = umma_desc_k_sw128(sbase + S::W3);
-    const float* s_bias = reinterpret_cast<const float*>(smem + S::BIAS);  // b2[64], b3[16]
+    const uint64_t dW3 = umma_desc_k_sw128(sbase + S::W3), dW2B = umma_desc_k_sw128(sbase + S::W2B);
+    const float* s_bias = reinterpret_cast<const float*>(smem + S::BIAS);  // b2[64], [b2b[64]], b3[16]
     const uint64_t dX = umma_desc_k_sw128(tX), dH1 = umma_desc_k_sw128(tH1), dH2 = umma_desc_k_sw128(tH2);
     const uint64_t dG1 = umma_desc_k_sw128(tG1), dG2 = umma_desc_k_sw128(tG2), dD3 = umma_desc_k_sw128(tD3);
+    const uint64_t dHL = umma_desc_k_sw128(tHL), dG3 = umma_desc_k_sw128(tG3);
     // MN-major views: W^T operands and the stacked [X^T; H1^T], [X^T; H2^T], delta^T tiles
     const uint64_t mW1 = umma_desc_mn_sw128(sbase + S::W1, 8192), mW2 = umma_desc_mn_sw128(sbase + S::W2, 8192);
-    const uint64_t mW3 = umma_desc_mn_sw128(sbase + S::W3, 8192);
+    const uint64_t mW3 = umma_desc_mn_sw128(sbase + S::W3, 8192), mW2B = umma_desc_mn_sw128(sbase + S::W2B, 8192);
     const uint64_t mXH1 = umma_desc_mn_sw128(tX, tH1 - tX), mXH2 = umma_desc_mn_sw128(tX, tH2 - tX);
+    const uint64_t mXHL = umma_desc_mn_sw128(tX, tHL - tX);
     const uint64_t mG1 = umma_desc_mn_sw128(tG1, S::TILE), mG2 = umma_desc_mn_sw128(tG2, S::TILE);
+    const uint64_t mG3 = umma_desc_mn_sw128(tG3, S::TILE);
     const uint64_t mD3 = umma_desc_mn_sw128(tD3, S::TILE);
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
     constexpr uint32_t ID64_BT = idesc_f16(128, 64, false, true), ID48_BT = idesc_f16(128, 48, false, true);
@@ -387,8 +420,8 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
         }
     };
 
-    int tile = blockIdx.x * TRAIN_WG + slot;
-    const int tstride = gridDim.x * TRAIN_WG;
+    int tile = blockIdx.x * SLOTS + slot;
+    const int tstride = gridDim.x * SLOTS;
     Fetch F;
     if (tile < p.n_tiles) fetch(tile, F);
     for (; tile < p.n_tiles; tile += tstride) {
@@ -454,7 +487,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
         }
         if (tile + tstride < p.n_tiles) fetch(tile + tstride, F);  // next tile's loads in flight
         wait_mma();
-        auto hidden_epilogue = [&](uint32_t tH, uint32_t tG, bool bias) {
+        auto hidden_epilogue = [&](uint32_t tH, uint32_t tG, const float* bias) {
             uint32_t r[32];
             tmem_ld32(t_s + lane_off + 32 * h, r);
             tmem_wait_ld();
@@ -463,7 +496,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
             for (int i = 0; i < 16; ++i) {
                 float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
                 if (bias) {
-                    const float2 bb = *reinterpret_cast<const float2*>(s_bias + 32 * h + 2 * i);
+                    const float2 bb = *reinterpret_cast<const float2*>(bias + 32 * h + 2 * i);
                     z0 += bb.x;
                     z1 += bb.y;
                 }
@@ -479,7 +512,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
                 sts_row_chunk(tG, row, 4 * h + cc, gv[4 * cc], gv[4 * cc + 1], gv[4 * cc + 2], gv[4 * cc + 3]);
             }
         };
-        hidden_epilogue(tH1, tG1, false);
+        hidden_epilogue(tH1, tG1, nullptr);
         sync_slot();
         // Z2 = H1 W2^T + b2
         if (issuer) {
@@ -489,13 +522,24 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
             mma_commit(bar);
         }
         wait_mma();
-        hidden_epilogue(tH2, tG2, true);
+        hidden_epilogue(tH2, tG2, s_bias);
+        if constexpr (HM == 2) {  // Z3 = H2 W2b^T + b2b
+            sync_slot();
+            if (issuer) {
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH2 + 2 * kk, dW2B + 2 * kk, ID64, kk > 0);
+                mma_commit(bar);
+            }
+            wait_mma();
+            hidden_epilogue(tH3, tG3, s_bias + 64);
+        }
         sync_slot();
-        // Y = H2 W3^T + b3
+        // Y = H_last W3^T + b3
         if (issuer) {
             tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH2 + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
+            for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dHL + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
             mma_commit(bar);
         }
         wait_mma();
@@ -511,7 +555,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
                 float rf;
                 asm volatile("{\n\t.reg .f16 hh;\n\tmov.b16 hh, %1;\n\tcvt.f32.f16 %0, hh;\n\t}" : "=f"(rf)
                              : "h"((uint16_t)(rawref[o >> 1] >> (16 * (o & 1)))));
-                const float e = (valid && o < c) ? __uint_as_float(r[o]) + s_bias[HID + o] - rf : 0.0f;
+                const float e = (valid && o < c) ? __uint_as_float(r[o]) + s_bias[64 * HM + o] - rf : 0.0f;
                 loss_acc = fmaf(e, e, loss_acc);
                 d3[o] = 2.0f * e;
             }
@@ -520,7 +564,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
                           h2u(d3[14], d3[15]));
         }
         sync_slot();
-        // ---- t5: dH2 = d3 W3
+        // ---- t5: dH_last = d3 W3
         if (issuer) {
             tc_fence_after();
             mma_f16_ss(t_s, dD3, mW3, ID64_BT, 0);
@@ -547,7 +591,19 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
                 sts_row_chunk(tG, row, 4 * h + cc, o[0], o[1], o[2], o[3]);
             }
         };
-        delta_epilogue(tG2);  // G2 tile now holds delta2
+        delta_epilogue(tGL);  // the last G tile now holds its delta
+        if constexpr (HM == 2) {  // dH2 = d3h W2b ; delta2
+            sync_slot();
+            if (issuer) {
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    mma_f16_ss(t_s, dG3 + 2 * kk, mW2B + (uint64_t)(kk * 128), ID64_BT, kk > 0);
+                mma_commit(bar);
+            }
+            wait_mma();
+            delta_epilogue(tG2);
+        }
         sync_slot();
         // dH1 = d2 W2
         if (issuer) {
@@ -571,8 +627,14 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
             // the next tile fetches; bar2 is waited before the next tile overwrites the tiles
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-                mma_f16_ss(t_acc_b, mXH2 + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
+                mma_f16_ss(t_acc_b, mXHL + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
                            (!first || kk > 0) ? 1u : 0u);
+            if constexpr (HM == 2) {  // dW2b/db2b += [X^T; H2^T] delta3h
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_f16_ss(t_acc_m, mXH2 + (uint64_t)(kk * 128), mG3 + (uint64_t)(kk * 128), ID64_AB,
+                               (!first || kk > 0) ? 1u : 0u);
+            }
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
                 mma_f16_ss(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
@@ -690,12 +752,12 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
         tc_fence_after();
     }
     // ---- t6: the CTA's weight-gradient partial (unscaled, one per CTA, fixed order): slot 1
-    // parks its TMEM accumulators in the (now idle) SMEM tile area, slot 0 adds its own and
-    // writes the partial.  Half 0 handles the dW1/db1 columns [0, 64), half 1 the dW2/db2
-    // columns [64, 128) and the dW3/db3 accumulator.
+    // (depth 1) parks its TMEM accumulators in the (now idle) SMEM tile area, slot 0 adds its
+    // own and writes the partial.  Half 0 handles the dW1/db1 columns [0, 64) (and the middle
+    // layer's dW2b/db2b at depth 2), half 1 the dW2/db2 columns [64, 128) and dW3/db3.
     float* part = p.partial + (size_t)blockIdx.x * p.P;
     float* park = reinterpret_cast<float*>(smem + S::WEND) + row * 145;  // [128][144] (+1 pad)
-    constexpr int NV = 80;  // values per thread: half 0 uses 64, half 1 uses 64 + 16
+    constexpr int NV = HM == 1 ? 80 : 128;
     auto read_acc = [&](float (&v)[NV], bool have) {
 #pragma unroll
         for (int blk = 0; blk < 2; ++blk) {
@@ -705,14 +767,25 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[32 * blk + e] = have ? __uint_as_float(r[e]) : 0.0f;
         }
-        uint32_t r[16];
-        tmem_ld16(t_acc_b + lane_off, r);
-        tmem_wait_ld();
+        if (h == 1) {
+            uint32_t r[16];
+            tmem_ld16(t_acc_b + lane_off, r);
+            tmem_wait_ld();
 #pragma unroll
-        for (int o = 0; o < 16; ++o) v[64 + o] = (have && h == 1) ? __uint_as_float(r[o]) : 0.0f;
+            for (int o = 0; o < 16; ++o) v[64 + o] = have ? __uint_as_float(r[o]) : 0.0f;
+        } else if (HM == 2) {
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) {
+                uint32_t r[32];
+                tmem_ld32(t_acc_m + lane_off + 32 * blk, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[NV - 64 + 32 * blk + e] = have ? __uint_as_float(r[e]) : 0.0f;
+            }
+        }
     };
-    __syncthreads();  // both slots are done with their tiles before the area is reused
-    if (slot == 1) {
+    __syncthreads();  // every slot is done with its tiles before the area is reused
+    if (SLOTS == 2 && slot == 1) {
         float v[NV];
         read_acc(v, !first);
 #pragma unroll
@@ -728,19 +801,29 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
     if (slot == 0) {
         float v[NV];
         read_acc(v, !first);
+        if (SLOTS == 2) {
 #pragma unroll
-        for (int e = 0; e < 64; ++e) v[e] += park[64 * h + e];
-        if (h == 1) {
+            for (int e = 0; e < 64; ++e) v[e] += park[64 * h + e];
+            if (h == 1) {
 #pragma unroll
-            for (int o = 0; o < 16; ++o) v[64 + o] += park[128 + o];
+                for (int o = 0; o < 16; ++o) v[64 + o] += park[128 + o];
+            }
         }
-        const int P1 = D * HID, o2 = P1 + HID, o3 = o2 + HID * HID + HID;
+        // ABI offsets: W1, b1, W2, b2, [W2b, b2b], W3, b3
+        const int P1 = D * HID, o2 = P1 + HID, o2b = o2 + HID * HID + HID, o3 = P1 + HID + HM * (HID * HID + HID);
         const int m = row;  // stacked rows: [0,64) X features, [64,128) H units
         if (h == 0) {
 #pragma unroll
             for (int col = 0; col < 64; ++col) {
                 if (m < D) part[col * D + m] = v[col];       // dW1[j][i]
                 else if (m == D) part[P1 + col] = v[col];    // db1[j]
+            }
+            if constexpr (HM == 2) {
+#pragma unroll
+                for (int col = 0; col < 64; ++col) {
+                    if (m == D) part[o2b + HID * HID + col] = v[64 + col];            // db2b[j]
+                    else if (m >= 64) part[o2b + col * HID + (m - 64)] = v[64 + col];  // dW2b[j][i]
+                }
             }
         } else {
 #pragma unroll
@@ -765,7 +848,7 @@ __global__ void __launch_bounds__(TRAIN_WG * 256, 1) train_kernel(const __grid_c
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (tid < TRAIN_WG) p.loss_partial[blockIdx.x * TRAIN_WG + tid] = s_loss[tid];
+    if (tid < SLOTS) p.loss_partial[blockIdx.x * SLOTS + tid] = s_loss[tid];
     if (warp == 0) tmem_dealloc(*s_tmem, 512);
 }
 
@@ -775,6 +858,7 @@ struct ReduceArgs {
     size_t part_stride;
     const float* loss_partial;
     int nparts, P;
+    int nloss;  // loss partials (CTAs x slots)
     float inv_bc;
     float* grad;
     float* loss;
@@ -799,7 +883,7 @@ __device__ __forceinline__ float reduce_block(const ReduceArgs& r, int blk, int&
     for (int k = 0; k < RED_MAXK; ++k) t += v[k];
     s[g][px] = t;
     if (blk == 0) {
-        const int nl = r.nparts * TRAIN_WG;  // <= 2 * 256
+        const int nl = r.nloss;  // <= 2 * 256
         float l = 0.0f;
         if ((int)threadIdx.x < nl) l = r.loss_partial[threadIdx.x];
         if ((int)threadIdx.x + 256 < nl) l += r.loss_partial[threadIdx.x + 256];
@@ -962,9 +1046,9 @@ static int ilog2_t(int64_t v) {
 
 extern "C" ntc_status ntc_trainer_create(const ntc_desc* d, ntc_trainer** out) {
     if (!d || !out) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
-    if (!(d->c0 == 8 && d->b0 == 2 && d->c1 == 12 && d->b1 == 4) || d->hidden_mats != 1 ||
+    if (!(d->c0 == 8 && d->b0 == 2 && d->c1 == 12 && d->b1 == 4) || (d->hidden_mats != 1 && d->hidden_mats != 2) ||
         (d->activation != 0 && d->activation != 1))
-        return api_fail(NTC_ERR_UNSUPPORTED, "training kernel compiled for NTC 0.2, [D,64,64,c], hardGELU or GELU");
+        return api_fail(NTC_ERR_UNSUPPORTED, "training kernel compiled for NTC 0.2, depth 1 or 2, hardGELU or GELU");
     if (d->channels < 1 || d->channels > 16 || d->width < 8 || (d->width & (d->width - 1)) ||
         d->width > (1 << 15))
         return api_fail(NTC_ERR_INVALID_ARGUMENT, "bad texture dims");
@@ -974,10 +1058,10 @@ extern "C" ntc_status ntc_trainer_create(const ntc_desc* d, ntc_trainer** out) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t P = ntc_num_params(d);
-    cudaError_t e = cudaMalloc(&t->partial, sizeof(float) * P * t->num_sms * TRAIN_WG);
-    if (e == cudaSuccess) e = cudaMalloc(&t->loss_partial, sizeof(float) * t->num_sms * TRAIN_WG);
-    if (e == cudaSuccess) e = cudaMalloc(&t->wimg, TrainSmem::WEND);
-    if (e == cudaSuccess) e = cudaMemset(t->wimg, 0, TrainSmem::WEND);
+    cudaError_t e = cudaMalloc(&t->partial, sizeof(float) * P * t->num_sms);
+    if (e == cudaSuccess) e = cudaMalloc(&t->loss_partial, sizeof(float) * t->num_sms * TrainSmemT<1>::SLOTS);
+    if (e == cudaSuccess) e = cudaMalloc(&t->wimg, TRAIN_WEND_MAX);
+    if (e == cudaSuccess) e = cudaMemset(t->wimg, 0, TRAIN_WEND_MAX);
     if (e != cudaSuccess) {
         ntc_trainer_destroy(t);
         return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
@@ -1257,8 +1341,9 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         pp.params = buf->params;
         pp.D = 4 * d->c0 + d->c1 + 13;
         pp.c = d->channels;
+        pp.hm = d->hidden_mats;
         pp.wimg = t->wimg;
-        prep_kernel<<<pp.prep_blocks + (WIMG_ITEMS + 255) / 256, 256, 0, st>>>(pp);
+        prep_kernel<<<pp.prep_blocks + (wimg_items(pp.hm) + 255) / 256, 256, 0, st>>>(pp);
         // t1, t3-t7
         TrainParams tp;
         memset(&tp, 0, sizeof tp);
@@ -1313,16 +1398,19 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.P = (int32_t)P;
         if (const char* dbg = getenv("NTC_DEBUG_TRAIN")) tp.debug_flags = atoi(dbg);
         tp.freeze = hp->freeze_latents;
+        const int hm = d->hidden_mats, slots = hm == 1 ? TrainSmemT<1>::SLOTS : TrainSmemT<2>::SLOTS;
+        const uint32_t smem_bytes = hm == 1 ? TrainSmemT<1>::BYTES : TrainSmemT<2>::BYTES;
         const int grid = (int)std::min<int64_t>(std::min<int64_t>(t->num_sms, 8 * RED_MAXK),
-                                                (tiles + TRAIN_WG - 1) / TRAIN_WG);
-        auto* k = d->activation == 1 ? train_kernel<8, 12, 1> : train_kernel<8, 12, 0>;
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TrainSmem::BYTES);
+                                                (tiles + slots - 1) / slots);
+        auto* k = hm == 1 ? (d->activation == 1 ? train_kernel<8, 12, 1, 1> : train_kernel<8, 12, 0, 1>)
+                          : (d->activation == 1 ? train_kernel<8, 12, 1, 2> : train_kernel<8, 12, 0, 2>);
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
         if (e == cudaSuccess) {
-            k<<<grid, TRAIN_WG * 256, TrainSmem::BYTES, st>>>(tp);
+            k<<<grid, slots * 256, smem_bytes, st>>>(tp);
             // t6: deterministic cross-CTA reduction, scaled by 1/(B c); with APPLY in the same
             // call, t8 rides in the same launch (weights Adam'd as they are reduced)
-            const ReduceArgs ra{t->partial, (size_t)P, t->loss_partial, grid, (int)P, tp.inv_bc, buf->grad_par, loss,
-                                status};
+            const ReduceArgs ra{t->partial,  (size_t)P,  t->loss_partial, grid, (int)P, grid * slots,
+                                tp.inv_bc,   buf->grad_par, loss,         status};
             const int rblocks = (int)((P + 31) / 32);
             if ((flags & NTC_STEP_APPLY) && apply_buffers_ok(buf)) {
                 AdamParams a;

@@ -17,10 +17,10 @@ DEV = "cuda:0"
 REL = 1e-2
 
 
-def _setup(O, W, c, seed, mip, n_crops, crop, out_gain=1.0, activation=0):
-    d = Profile.named("ntc0.2", W, c, activation=activation)
+def _setup(O, W, c, seed, mip, n_crops, crop, out_gain=1.0, activation=0, hidden_mats=1):
+    d = Profile.named("ntc0.2", W, c, hidden_mats, activation)
     lat = gen_latents(seed, O.num_latents(d))
-    par = gen_weights_f32(seed + 1, d.input_dim, c, out_gain=out_gain)
+    par = gen_weights_f32(seed + 1, d.input_dim, c, hidden_mats, out_gain=out_gain)
     chain = box_mip_chain_u8(gen_reference_u8(seed + 2, W, c))
     ref = u8_to_f16_bits(chain[mip])
     crops = gen_crops(seed + 3, W, mip, n_crops, crop)
@@ -53,7 +53,10 @@ def _gpu_grads(O, d, lat, par, ref, crops, mip, seed, step, noise_on=True):
 
 def _param_slices(d):
     D, c = d.input_dim, d.channels
-    names, sizes = ["W1", "b1", "W2", "b2", "W3", "b3"], [64 * D, 64, 4096, 64, 64 * c, c]
+    names, sizes = ["W1", "b1", "W2", "b2"], [64 * D, 64, 4096, 64]
+    if d.hidden_mats == 2:
+        names, sizes = names + ["W2b", "b2b"], sizes + [4096, 64]
+    names, sizes = names + ["W3", "b3"], sizes + [64 * c, c]
     out, o = {}, 0
     for n, s in zip(names, sizes):
         out[n] = slice(o, o + s)
@@ -101,6 +104,17 @@ def test_train_grads_gelu(O, mip, n_crops, crop):
     d, lat, par, ref, crops = _setup(O, 64, 9, 40 + mip, mip, n_crops, crop, activation=1)
     loss, gp, gl, _ = _gpu_grads(O, d, lat, par, ref, crops, mip, 41, 2)
     loss_o, dp, dl = O.train_grads(d, lat, par, mip, crops, ref, 41, 2)
+    assert abs(loss - loss_o) <= 1e-3 * loss_o
+    _check_all(O, d, gp, gl, dp, dl)
+
+
+@pytest.mark.parametrize("mip,n_crops,crop,act", [(0, 2, 32, 0), (2, 3, 8, 0), (0, 2, 24, 1)])
+def test_train_grads_depth2(O, mip, n_crops, crop, act):
+    """f4: depth reading B ([D,64,64,64,c], hidden_mats = 2, R11) of the training step (one
+    slot per CTA): loss and every gradient tensor, including W2b/b2b, vs the oracle."""
+    d, lat, par, ref, crops = _setup(O, 64, 9, 60 + mip, mip, n_crops, crop, activation=act, hidden_mats=2)
+    loss, gp, gl, _ = _gpu_grads(O, d, lat, par, ref, crops, mip, 61, 3)
+    loss_o, dp, dl = O.train_grads(d, lat, par, mip, crops, ref, 61, 3)
     assert abs(loss - loss_o) <= 1e-3 * loss_o
     _check_all(O, d, gp, gl, dp, dl)
 
