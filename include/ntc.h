@@ -43,8 +43,7 @@ typedef enum {
  * decoder MLP [D, 64, 64, c] (hidden_mats = 1) or [D, 64, 64, 64, c]
  * (hidden_mats = 2, reading R11), D = 4C0 + C1 + 12 + 1, hardGELU
  * (activation = 0) or exact GELU x Phi(x) (activation = 1, PAPER.md:496;
- * decode: every profile/depth; training: NTC 0.2, both depths).  Compiled profiles: NTC
- * 0.2/0.5/1.0/2.25 (training: NTC 0.2).                                                    */
+ * decode and training).  Compiled profiles: NTC 0.2/0.5/1.0/2.25, depth 1 or 2.           */
 typedef struct {
     int32_t width;
     int32_t channels;

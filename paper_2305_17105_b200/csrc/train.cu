@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -104,26 +105,30 @@ __device__ __forceinline__ void box_locate(const Box* box, const int32_t* start,
 }
 
 // ------------------------------------------------------------------ fused forward + backward
-// SMEM layout for depth HM (1: [D,64,64,c]; 2: [D,64,64,64,c], R11): fp16 weight images (W1 with
-// b1 at column D, W2, [W2b], W3 with 16 rows) + fp32 biases b2[64], [b2b[64]], b3[16]; then per
-// tile pipeline ("slot") the SW128 activation tiles.  Depth 2 needs 8 tiles per slot, which
-// leaves SMEM for one slot.
-template <int HM>
+// SMEM layout for depth HM (1: [D,64,64,c]; 2: [D,64,64,64,c], R11) and KA 64-column K atoms
+// of X (1: K1 = 64, NTC 0.2; 2: K1 = 80/96, the other Table 2 profiles): fp16 weight images
+// (W1 in KA atoms with b1 at column D, W2, [W2b], W3 with 16 rows) + fp32 biases b2[64],
+// [b2b[64]], b3[16]; then per tile pipeline ("slot") the SW128 activation tiles.  Only the
+// depth-1 K1 = 64 layout leaves SMEM for two slots.
+template <int HM, int KA = 1>
 struct TrainSmemT {
-    static constexpr uint32_t W1 = 0, W2 = 8192, W2B = 16384, W3 = 8192u * (1 + HM), BIAS = W3 + 2048;
+    static constexpr uint32_t W1 = 0, W2 = 8192u * KA, W2B = W2 + 8192, W3 = W2 + 8192u * HM, BIAS = W3 + 2048;
     static constexpr uint32_t NBIAS = 64 * HM + 16;
     static constexpr uint32_t WEND = ((BIAS + 4 * NBIAS + 1023) / 1024) * 1024;
     static constexpr uint32_t TILE = 128 * 128;  // one 128 x 64 fp16 SW128 tile
-    // G1 and G2 adjacent: [delta1 | delta2] is one N=128 operand of the weight-gradient MMA
-    // depth 1: X H1 H2 G1 G2 D3; depth 2: X H1 H2 H3 G1 G2 G3 D3
-    enum { X = 0, H1 = 1, H2 = 2, H3 = 3, G1 = 2 + HM, G2 = 3 + HM, G3 = 6, D3 = 3 + 2 * HM, NT = 4 + 2 * HM };
-    static constexpr int SLOTS = HM == 1 ? 2 : 1;
+    // depth 1: X[KA] H1 H2 G1 G2 D3; depth 2: X[KA] H1 H2 H3 G1 G2 G3 D3
+    // (G1 and G2 adjacent: [delta1 | delta2] is one N=128 operand of the weight-gradient MMA)
+    enum {
+        X = 0, H1 = KA, H2 = KA + 1, H3 = KA + 2, G1 = KA + 1 + HM, G2 = KA + 2 + HM, G3 = KA + 5,
+        D3 = KA + 2 + 2 * HM, NT = KA + 3 + 2 * HM
+    };
+    static constexpr int SLOTS = (HM == 1 && KA == 1) ? 2 : 1;
     static constexpr uint32_t WG_BYTES = NT * TILE;
     static constexpr uint32_t MISC = 256 + 16 * NTC_MAX_CROPS + 4 * (NTC_MAX_CROPS + 1) + 12;
     static constexpr uint32_t BYTES = 1024 + WEND + SLOTS * WG_BYTES + MISC;
 };
 using TrainSmem = TrainSmemT<1>;
-constexpr uint32_t TRAIN_WEND_MAX = TrainSmemT<2>::WEND;
+constexpr uint32_t TRAIN_WEND_MAX = TrainSmemT<2, 2>::WEND;
 
 __device__ __forceinline__ void sts_row_chunk(uint32_t tile, int row, int chunk, uint32_t a, uint32_t b, uint32_t c,
                                               uint32_t d) {
@@ -151,23 +156,27 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                  : "memory");
 }
 
+__device__ __forceinline__ void red_add_v2(float* p, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+
 __device__ __forceinline__ uint32_t h2u(float a, float b) { return pack_half2(a, b); }
 
 // fp16 SW128 weight image of the current fp32 master weights (t3): W1 (+ b1 at column D, it
 // multiplies X's constant 1), W2, [W2b], W3 (16 rows); the hidden and output biases as fp32
 // values of their fp16 rounding (R14), added in the epilogues.  ABI parameter order: W1, b1,
 // W2, b2, [W2b, b2b], W3, b3.
-__host__ __device__ constexpr int wimg_items(int hm) { return (2 + hm) * 4096 + 64 * hm + 16; }
-template <int HM>
+__host__ __device__ constexpr int wimg_items(int hm, int ka) { return (1 + ka + hm) * 4096 + 64 * hm + 16; }
+template <int HM, int KA>
 __device__ __forceinline__ void train_wimg_item_t(int i, const float* __restrict__ w, int D, int c,
                                                   uint8_t* __restrict__ img) {
-    using S = TrainSmemT<HM>;
-    if (i >= wimg_items(HM)) return;
+    using S = TrainSmemT<HM, KA>;
+    if (i >= wimg_items(HM, KA)) return;
     const int P1 = D * HID;                  // b1
     const int o3 = P1 + HID + HM * (HID * HID + HID);  // W3
     float* bias = reinterpret_cast<float*>(img + S::BIAS);
-    if (i >= (2 + HM) * 4096) {
-        const int j = i - (2 + HM) * 4096;
+    if (i >= (1 + KA + HM) * 4096) {
+        const int j = i - (1 + KA + HM) * 4096;
         if (j < 64 * HM) {  // hidden biases b2 (, b2b)
             const int l = j / 64, o = j % 64;
             bias[j] = __half2float(__float2half_rn(w[P1 + HID + l * (HID * HID + HID) + HID * HID + o]));
@@ -177,21 +186,23 @@ __device__ __forceinline__ void train_wimg_item_t(int i, const float* __restrict
         }
         return;
     }
-    const int part = i / 4096, e = i % 4096, r = e / 64, k = e % 64;
+    const int part = i / 4096, e = i % 4096, r = e / 64, kk = e % 64;
     float v = 0.0f;
     uint32_t base;
-    if (part == 0) {
+    if (part < KA) {  // W1 atom `part`: X features 64 part + kk
+        const int k = 64 * part + kk;
         v = k < D ? w[r * D + k] : (k == D ? w[P1 + r] : 0.0f);
-        base = S::W1;
-    } else if (part <= HM) {  // hidden matrix part-1
-        v = w[P1 + HID + (part - 1) * (HID * HID + HID) + r * HID + k];
-        base = part == 1 ? S::W2 : S::W2B;
+        base = S::W1 + 8192u * part;
+    } else if (part < KA + HM) {  // hidden matrix
+        const int l = part - KA;
+        v = w[P1 + HID + l * (HID * HID + HID) + r * HID + kk];
+        base = l == 0 ? S::W2 : S::W2B;
     } else {
         if (r >= 16) return;
-        v = r < c ? w[o3 + r * HID + k] : 0.0f;
+        v = r < c ? w[o3 + r * HID + kk] : 0.0f;
         base = S::W3;
     }
-    *reinterpret_cast<__half*>(img + base + sw128_offset(r, k)) = __float2half_rn(v);
+    *reinterpret_cast<__half*>(img + base + sw128_offset(r, kk)) = __float2half_rn(v);
 }
 
 // t2: noisy = latent + U(-Q/2, Q/2) (one draw per latent per step), grad = 0, over the footprint
@@ -199,10 +210,13 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
     if ((int)blockIdx.x >= p.prep_blocks) {
         const int i = ((int)blockIdx.x - p.prep_blocks) * blockDim.x + threadIdx.x;
         if (p.wimg) {
+            const bool ka2 = p.D + 1 > 64;
             if (p.hm == 2)
-                train_wimg_item_t<2>(i, p.params, p.D, p.c, p.wimg);
+                ka2 ? train_wimg_item_t<2, 2>(i, p.params, p.D, p.c, p.wimg)
+                    : train_wimg_item_t<2, 1>(i, p.params, p.D, p.c, p.wimg);
             else
-                train_wimg_item_t<1>(i, p.params, p.D, p.c, p.wimg);
+                ka2 ? train_wimg_item_t<1, 2>(i, p.params, p.D, p.c, p.wimg)
+                    : train_wimg_item_t<1, 1>(i, p.params, p.D, p.c, p.wimg);
         }
         return;
     }
@@ -240,19 +254,30 @@ __device__ __forceinline__ void act_and_grad(float z, float& h, float& g) {
     }
 }
 
-template <int C0, int C1, int ACT, int HM>
-__global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(const __grid_constant__ TrainParams p) {
+template <class P> struct TrainGeom {
+    static constexpr int C0 = P::C0, C1 = P::C1;
+    static constexpr int D = 4 * C0 + C1 + 13, NLAT = 4 * C0 + C1;
+    static constexpr int K1 = ((D + 1 + 15) / 16) * 16, KA = (K1 + 63) / 64;
+};
+
+template <class P, int ACT, int HM>
+__global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256, 1)
+    train_kernel(const __grid_constant__ TrainParams p) {
     // Two independent tile pipelines ("slots") per CTA, 8 warps each.  The 4 TMEM lane
     // quarters of a 128-texel tile are served by two warps each that split the columns: half
     // h = 0 owns columns [0, 32) of every 64-wide activation (and the G0 part of X / dX, the
     // reference texels and the loss), half h = 1 columns [32, 64) (and the G1 / PE / LOD part).
     // Depth HM = 2 ([D,64,64,64,c], R11) adds a hidden layer (H3/G3 tiles, one more forward
     // and backward round trip, a third weight-gradient stack) and runs one slot per CTA.
-    using S = TrainSmemT<HM>;
+    // KA = 2 (the K1 = 80/96 profiles): X spans two K atoms; the weight gradients of W1 come
+    // from the stack [X0^T; X1^T], the biases b2/b2b/b3 through the constant column D in X1.
+    using G = TrainGeom<P>;
+    constexpr int C0 = G::C0, C1 = G::C1, D = G::D, NLAT = G::NLAT, K1 = G::K1, KA = G::KA;
+    using S = TrainSmemT<HM, KA>;
     constexpr int SLOTS = S::SLOTS;
-    constexpr int D = 4 * C0 + C1 + 13;
-    constexpr int NLAT = 4 * C0 + C1;   // latent columns of X
-    static_assert(D < 64 && NLAT <= 48 && 4 * C0 == 32, "training kernel: K1 = 64, 32 G0 columns");
+    constexpr int NLATP = ((NLAT + 15) / 16) * 16;  // dX columns (MMA N)
+    constexpr int DX = D - 64 * (KA - 1);           // row of the constant column in the stacked X block
+    static_assert(C0 % 4 == 0 && C1 % 2 == 0 && NLATP <= 128 && KA <= 2, "training kernel profile");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::WEND + SLOTS * S::WG_BYTES);
@@ -291,7 +316,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
     // depth 2: [0,128) dW-a, [128,192) dW-m (the middle layer), [192,208) dW-b, [256,320) scratch
     const uint32_t tbase = *s_tmem + (uint32_t)slot * (512u / SLOTS);
     const uint32_t t_acc_a = tbase, t_acc_m = tbase + 128, t_acc_b = tbase + (HM == 1 ? 128 : 192);
-    const uint32_t t_s = tbase + (HM == 1 ? 192 : 256);
+    const uint32_t t_s = tbase + (SLOTS == 2 ? 192 : 256);  // 64 (two slots) or 128 scratch columns
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t sbase = smem_u32(smem);
     const uint32_t tiles = sbase + S::WEND + (uint32_t)slot * S::WG_BYTES;
@@ -299,6 +324,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
     const uint32_t tG1 = tiles + S::G1 * S::TILE, tG2 = tiles + S::G2 * S::TILE, tD3 = tiles + S::D3 * S::TILE;
     const uint32_t tH3 = tiles + S::H3 * S::TILE, tG3 = tiles + S::G3 * S::TILE;  // depth 2 only
     const uint32_t tHL = HM == 1 ? tH2 : tH3, tGL = HM == 1 ? tG2 : tG3;        // last hidden layer
+    const uint32_t tXB = tX + (uint32_t)(KA - 1) * S::TILE;  // X atom holding the constant column D
     const bool issuer = (warp & 7) == slot * 2 && lane == 0;  // the two issuers on different sub-partitions
     uint64_t* bar = &s_bar[slot];
     uint64_t* bar2 = &s_bar[SLOTS + slot];
@@ -323,13 +349,14 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
     // MN-major views: W^T operands and the stacked [X^T; H1^T], [X^T; H2^T], delta^T tiles
     const uint64_t mW1 = umma_desc_mn_sw128(sbase + S::W1, 8192), mW2 = umma_desc_mn_sw128(sbase + S::W2, 8192);
     const uint64_t mW3 = umma_desc_mn_sw128(sbase + S::W3, 8192), mW2B = umma_desc_mn_sw128(sbase + S::W2B, 8192);
-    const uint64_t mXH1 = umma_desc_mn_sw128(tX, tH1 - tX), mXH2 = umma_desc_mn_sw128(tX, tH2 - tX);
-    const uint64_t mXHL = umma_desc_mn_sw128(tX, tHL - tX);
+    const uint64_t mXH1 = umma_desc_mn_sw128(tXB, tH1 - tXB), mXH2 = umma_desc_mn_sw128(tXB, tH2 - tXB);
+    const uint64_t mXHL = umma_desc_mn_sw128(tXB, tHL - tXB);
+    const uint64_t mXX = umma_desc_mn_sw128(tX, S::TILE);  // KA = 2: [X0^T; X1^T]
     const uint64_t mG1 = umma_desc_mn_sw128(tG1, S::TILE), mG2 = umma_desc_mn_sw128(tG2, S::TILE);
     const uint64_t mG3 = umma_desc_mn_sw128(tG3, S::TILE);
     const uint64_t mD3 = umma_desc_mn_sw128(tD3, S::TILE);
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
-    constexpr uint32_t ID64_BT = idesc_f16(128, 64, false, true), ID48_BT = idesc_f16(128, 48, false, true);
+    constexpr uint32_t ID64_BT = idesc_f16(128, 64, false, true), IDX_BT = idesc_f16(128, NLATP, false, true);
     constexpr uint32_t ID64_AB = idesc_f16(128, 64, true, true), ID16_AB = idesc_f16(128, 16, true, true);
 
     float loss_acc = 0.0f;
@@ -372,13 +399,34 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
         ty[0] = max(j, 0);
         ty[1] = min(j + 1, p.r1 - 1);
     };
-    // ---- t2 fetch, one tile ahead: half 0 the four fp16 G0 cells (4 x 16 B), half 1 the four
-    // fp16 G1 cells (4 x 24 B) and the raw reference texel (one register array serves both)
-    static_assert(C0 == 8 && C1 == 12, "fetch layout: 16-byte G0 cells, 24-byte G1 cells");
+    // ---- t2 fetch, one tile ahead: half 0 the four fp16 G0 cells (4 x C0 halves) and the raw
+    // reference texel, half 1 the four fp16 G1 cells (4 x C1 halves); one register array
+    // serves both halves
+    constexpr int NVW = 2 * (C0 > C1 ? C0 : C1);  // 32-bit words: 4 cells x C/2
     struct Fetch {
         Texel t;
-        uint32_t v[24];    // h = 0: G0 taps (4 x uint4); h = 1: G1 taps (4 x 3 x uint2)
+        uint32_t v[NVW];   // h = 0: G0 taps (tap-major, 2 C0 words); h = 1: G1 taps (2 C1 words)
         uint32_t ref[8];   // h = 0: reference channels (fp16 pairs)
+    };
+    // one fp16 cell of C channels (C/2 words) with the widest aligned vector loads
+    auto load_cell_h = [&](const __half* cell, int C, uint32_t* out) {
+        if (C % 8 == 0) {
+            for (int e = 0; e < C / 8; ++e) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(cell) + e);
+                out[4 * e] = v.x;
+                out[4 * e + 1] = v.y;
+                out[4 * e + 2] = v.z;
+                out[4 * e + 3] = v.w;
+            }
+        } else if (C % 4 == 0) {
+            for (int e = 0; e < C / 4; ++e) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(cell) + e);
+                out[2 * e] = v.x;
+                out[2 * e + 1] = v.y;
+            }
+        } else {
+            for (int e = 0; e < C / 2; ++e) out[e] = __ldg(reinterpret_cast<const uint32_t*>(cell) + e);
+        }
     };
     auto fetch = [&](int tile, Fetch& f) {
         f.t = texel_of(tile);
@@ -387,13 +435,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
             taps_g0(f.t, tx, ty);
             const __half* g0 = p.noisy + p.off0;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(g0 + (ty[t >> 1] * p.r0 + tx[t & 1]) * C0));
-                f.v[4 * t] = v.x;
-                f.v[4 * t + 1] = v.y;
-                f.v[4 * t + 2] = v.z;
-                f.v[4 * t + 3] = v.w;
-            }
+            for (int t = 0; t < 4; ++t) load_cell_h(g0 + (ty[t >> 1] * p.r0 + tx[t & 1]) * C0, C0, f.v + t * (C0 / 2));
             const uint16_t* rp = p.ref + (int64_t)f.t.y * p.ref_stride + (int64_t)f.t.x * c;
 #pragma unroll
             for (int o = 0; o < 8; ++o) {
@@ -408,15 +450,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
             taps_g1(f.t, tx, ty, ax, ay);
             const __half* g1 = p.noisy + p.off1;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const uint2* c1 = reinterpret_cast<const uint2*>(g1 + (ty[t >> 1] * p.r1 + tx[t & 1]) * C1);
-#pragma unroll
-                for (int e = 0; e < 3; ++e) {
-                    const uint2 v = __ldg(c1 + e);
-                    f.v[6 * t + 2 * e] = v.x;
-                    f.v[6 * t + 2 * e + 1] = v.y;
-                }
-            }
+            for (int t = 0; t < 4; ++t) load_cell_h(g1 + (ty[t >> 1] * p.r1 + tx[t & 1]) * C1, C1, f.v + t * (C1 / 2));
         }
     };
 
@@ -430,12 +464,16 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
         uint32_t rawref[8];
 #pragma unroll
         for (int o = 0; o < 8; ++o) rawref[o] = F.ref[o];
-        // ---- a2-a4: this half's 32 columns of the X row (canonical order, R4) -> SW128 tile
+        // ---- a2-a4: this half's part of the X row (canonical order, R4) -> SW128 tile(s): half 0
+        // the G0 words [0, 2 C0), half 1 the G1 bilinear, PE, LOD + bias one and the padding up
+        // to K1; both parts start on a 16-byte chunk (2 C0 is a multiple of 4 words)
         {
-            uint32_t xw[16];
+            constexpr int W0 = 2 * C0, W1N = K1 / 2 - 2 * C0;  // words of half 0 / half 1
+            constexpr int XW = W0 > W1N ? W0 : W1N;
+            uint32_t xw[XW];
             if (h == 0) {  // G0 taps: the fp16 noisy latents are X
 #pragma unroll
-                for (int i = 0; i < 16; ++i) xw[i] = F.v[i];
+                for (int i = 0; i < W0; ++i) xw[i] = F.v[i];
             } else {       // G1 bilinear in fp32 from the fp16 taps, rounded once; PE; LOD
                 int tx[2], ty[2];
                 uint32_t ax, ay;
@@ -449,14 +487,14 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
                     const float wf = (float)wq[t] * (1.0f / 256.0f);
 #pragma unroll
                     for (int e = 0; e < C1 / 2; ++e) {
-                        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&F.v[6 * t + e]));
-                        acc[2 * e + 0] = fmaf(wf, a.x, acc[2 * e + 0]);
-                        acc[2 * e + 1] = fmaf(wf, a.y, acc[2 * e + 1]);
+                        const float2 a2 = __half22float2(*reinterpret_cast<const __half2*>(&F.v[t * (C1 / 2) + e]));
+                        acc[2 * e + 0] = fmaf(wf, a2.x, acc[2 * e + 0]);
+                        acc[2 * e + 1] = fmaf(wf, a2.y, acc[2 * e + 1]);
                     }
                 }
 #pragma unroll
                 for (int e = 0; e < C1; e += 2) xw[e / 2] = h2u(acc[e], acc[e + 1]);
-                constexpr int PEW = NLAT / 2 - 16;  // word index inside this half
+                constexpr int PEW = C1 / 2;  // word index inside this half
                 xw[PEW + 0] = s_pe[4 * (T.x & 7) + 0];
                 xw[PEW + 1] = s_pe[4 * (T.x & 7) + 1];
                 xw[PEW + 2] = s_pe[4 * (T.x & 7) + 2];
@@ -465,7 +503,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
                 xw[PEW + 5] = s_pe[4 * (T.y & 7) + 2];
                 xw[PEW + 6] = p.lod_word;
 #pragma unroll
-                for (int e = PEW + 7; e < 16; ++e) xw[e] = 0u;
+                for (int e = PEW + 7; e < W1N; ++e) xw[e] = 0u;
             }
             if (pending_w) {  // the previous tile's weight-gradient MMAs still read the tiles
                 mbar_wait(bar2, phase2);
@@ -473,16 +511,24 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
                 tc_fence_after();
                 pending_w = false;
             }
+            const int ch0 = h == 0 ? 0 : W0 / 4, nch = (h == 0 ? W0 : W1N) / 4;
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch)
-                sts_row_chunk(tX, row, 4 * h + ch, xw[4 * ch], xw[4 * ch + 1], xw[4 * ch + 2], xw[4 * ch + 3]);
+            for (int ch = 0; ch < XW / 4; ++ch) {
+                if (ch < nch) {
+                    const int g = ch0 + ch;  // chunk of the K1-wide row: atom g / 8, chunk g % 8
+                    sts_row_chunk(tX + (uint32_t)(g >> 3) * S::TILE, row, g & 7, xw[4 * ch], xw[4 * ch + 1],
+                                  xw[4 * ch + 2], xw[4 * ch + 3]);
+                }
+            }
         }
         sync_slot();
         // ---- t3: forward.  Z1 = X W1^T (+b1)
         if (issuer) {
             tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dX + 2 * kk, dW1 + 2 * kk, ID64, kk > 0);
+            for (int kk = 0; kk < K1 / 16; ++kk)
+                mma_f16_ss(t_s, dX + (uint64_t)(((kk >> 2) * S::TILE + (kk & 3) * 32) >> 4),
+                           dW1 + (uint64_t)(((kk >> 2) * 8192 + (kk & 3) * 32) >> 4), ID64, kk > 0);
             mma_commit(bar);
         }
         if (tile + tstride < p.n_tiles) fetch(tile + tstride, F);  // next tile's loads in flight
@@ -621,7 +667,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                mma_f16_ss(t_s, dG1 + 2 * kk, mW1 + (uint64_t)(kk * 128), ID48_BT, kk > 0);
+                mma_f16_ss(t_s, dG1 + 2 * kk, mW1 + (uint64_t)(kk * 128), IDX_BT, kk > 0);
             mma_commit(bar);
             // weight gradients, off the critical path: they run while this tile scatters and
             // the next tile fetches; bar2 is waited before the next tile overwrites the tiles
@@ -639,9 +685,11 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
             for (int kk = 0; kk < 8; ++kk)
                 mma_f16_ss(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
                            (!first || kk > 0) ? 1u : 0u);
+            // dW1/db1: [X^T; H1^T] delta1 (K1 = 64: rows 64-127 unused) or [X0^T; X1^T] delta1
+            const uint64_t mA1 = KA == 1 ? mXH1 : mXX;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-                mma_f16_ss(t_acc_a, mXH1 + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID64_AB,
+                mma_f16_ss(t_acc_a, mA1 + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID64_AB,
                            (!first || kk > 0) ? 1u : 0u);
             mma_commit(bar2);
         }
@@ -657,24 +705,30 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
             const float s = p.inv_bc;
             const bool on = valid && !(p.debug_flags & 1) && !p.freeze;
             if (h == 0) {
-                uint32_t r[32];
-                tmem_ld32(t_s + lane_off, r);
-                tmem_wait_ld();
+                uint32_t r[4 * C0];
+#pragma unroll
+                for (int blk = 0; blk < C0 / 4; ++blk) {
+                    uint32_t q16[16];
+                    tmem_ld16(t_s + lane_off + 16 * blk, q16);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) r[16 * blk + e] = q16[e];
+                }
                 int tx0[2], ty0[2];
                 taps_g0(T, tx0, ty0);
                 float* gl0 = p.grad_lat + p.off0;
                 const uint32_t kx0 = on ? (uint32_t)(tx0[0] | (tx0[1] << 16)) : 0xFFFFFFF0u - lane;
                 const uint32_t ky0 = (uint32_t)(ty0[0] | (ty0[1] << 16));
-                float g0v[32];
+                float g0v[4 * C0];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) g0v[i] = on ? __uint_as_float(r[i]) : 0.0f;
+                for (int i = 0; i < 4 * C0; ++i) g0v[i] = on ? __uint_as_float(r[i]) : 0.0f;
 #pragma unroll
                 for (int d = 1; d <= 2; d <<= 1) {
                     const uint32_t nx0 = __shfl_down_sync(0xffffffffu, kx0, d);
                     const uint32_t ny0 = __shfl_down_sync(0xffffffffu, ky0, d);
                     const bool s0 = lane + d < 32 && nx0 == kx0 && ny0 == ky0;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
+                    for (int i = 0; i < 4 * C0; ++i) {
                         const float o = __shfl_down_sync(0xffffffffu, g0v[i], d);
                         if (s0) g0v[i] += o;
                     }
@@ -692,8 +746,12 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
                     }
                 }
             } else {
-                uint32_t r[16];
-                tmem_ld16(t_s + lane_off + 32, r);
+                constexpr int NR = C1 <= 16 ? 16 : 32;
+                uint32_t r[NR];
+                if constexpr (NR == 16)
+                    tmem_ld16(t_s + lane_off + 4 * C0, r);
+                else
+                    tmem_ld32(t_s + lane_off + 4 * C0, r);
                 tmem_wait_ld();
                 int tx1[2], ty1[2];
                 uint32_t axq, ayq;
@@ -735,9 +793,14 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
                         float* dst = gl1 + ((int64_t)ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1;
                         const float sw = s * wy;
                         if (sw != 0.0f) {
+                            if constexpr (C1 % 4 == 0) {
 #pragma unroll
-                            for (int e = 0; e < C1; e += 4)
-                                red_add_v4(dst + e, sw * Sv[e], sw * Sv[e + 1], sw * Sv[e + 2], sw * Sv[e + 3]);
+                                for (int e = 0; e < C1; e += 4)
+                                    red_add_v4(dst + e, sw * Sv[e], sw * Sv[e + 1], sw * Sv[e + 2], sw * Sv[e + 3]);
+                            } else {  // 8-byte aligned cells (C1 = 10)
+#pragma unroll
+                                for (int e = 0; e < C1; e += 2) red_add_v2(dst + e, sw * Sv[e], sw * Sv[e + 1]);
+                            }
                         }
                     }
                 }
@@ -811,7 +874,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
         }
         // ABI offsets: W1, b1, W2, b2, [W2b, b2b], W3, b3
         const int P1 = D * HID, o2 = P1 + HID, o2b = o2 + HID * HID + HID, o3 = P1 + HID + HM * (HID * HID + HID);
-        const int m = row;  // stacked rows: [0,64) X features, [64,128) H units
+        const int m = row;  // stacked rows: X features (64 per atom), then H units at [64,128)
         if (h == 0) {
 #pragma unroll
             for (int col = 0; col < 64; ++col) {
@@ -821,20 +884,20 @@ __global__ void __launch_bounds__(TrainSmemT<HM>::SLOTS * 256, 1) train_kernel(c
             if constexpr (HM == 2) {
 #pragma unroll
                 for (int col = 0; col < 64; ++col) {
-                    if (m == D) part[o2b + HID * HID + col] = v[64 + col];            // db2b[j]
+                    if (m == DX) part[o2b + HID * HID + col] = v[64 + col];           // db2b[j]
                     else if (m >= 64) part[o2b + col * HID + (m - 64)] = v[64 + col];  // dW2b[j][i]
                 }
             }
         } else {
 #pragma unroll
             for (int col = 0; col < 64; ++col) {
-                if (m == D) part[o2 + HID * HID + col] = v[col];            // db2[j]
+                if (m == DX) part[o2 + HID * HID + col] = v[col];           // db2[j]
                 else if (m >= 64) part[o2 + col * HID + (m - 64)] = v[col];  // dW2[j][i]
             }
 #pragma unroll
             for (int o = 0; o < 16; ++o) {
                 if (o >= c) continue;
-                if (m == D) part[o3 + HID * c + o] = v[64 + o];                // db3[o]
+                if (m == DX) part[o3 + HID * c + o] = v[64 + o];               // db3[o]
                 else if (m >= 64) part[o3 + o * HID + (m - 64)] = v[64 + o];   // dW3[o][i]
             }
         }
@@ -1044,11 +1107,39 @@ static int ilog2_t(int64_t v) {
     return l;
 }
 
+// compiled training profiles (Table 2) and the kernel instantiation of (profile, act, depth)
+static int train_profile(const ntc_desc* d) {
+    if (d->c0 == 8 && d->b0 == 2 && d->c1 == 12 && d->b1 == 4) return 0;
+    if (d->c0 == 12 && d->b0 == 4 && d->c1 == 20 && d->b1 == 4) return 1;
+    if (d->c0 == 12 && d->b0 == 2 && d->c1 == 10 && d->b1 == 4) return 2;
+    if (d->c0 == 16 && d->b0 == 4 && d->c1 == 12 && d->b1 == 4) return 3;
+    return -1;
+}
+
+template <class F>
+static void train_dispatch(const ntc_desc* d, F&& f) {
+    auto with_ah = [&](auto pr) {
+        const bool g = d->activation == 1;
+        if (d->hidden_mats == 2)
+            g ? f(pr, std::integral_constant<int, 1>{}, std::integral_constant<int, 2>{})
+              : f(pr, std::integral_constant<int, 0>{}, std::integral_constant<int, 2>{});
+        else
+            g ? f(pr, std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{})
+              : f(pr, std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
+    };
+    switch (train_profile(d)) {
+        case 0: with_ah(Prof<8, 2, 12, 4>{}); break;
+        case 1: with_ah(Prof<12, 4, 20, 4>{}); break;
+        case 2: with_ah(Prof<12, 2, 10, 4>{}); break;
+        default: with_ah(Prof<16, 4, 12, 4>{}); break;
+    }
+}
+
 extern "C" ntc_status ntc_trainer_create(const ntc_desc* d, ntc_trainer** out) {
     if (!d || !out) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
-    if (!(d->c0 == 8 && d->b0 == 2 && d->c1 == 12 && d->b1 == 4) || (d->hidden_mats != 1 && d->hidden_mats != 2) ||
+    if (train_profile(d) < 0 || (d->hidden_mats != 1 && d->hidden_mats != 2) ||
         (d->activation != 0 && d->activation != 1))
-        return api_fail(NTC_ERR_UNSUPPORTED, "training kernel compiled for NTC 0.2, depth 1 or 2, hardGELU or GELU");
+        return api_fail(NTC_ERR_UNSUPPORTED, "training kernel compiled for the Table 2 profiles, depth 1 or 2, hardGELU or GELU");
     if (d->channels < 1 || d->channels > 16 || d->width < 8 || (d->width & (d->width - 1)) ||
         d->width > (1 << 15))
         return api_fail(NTC_ERR_INVALID_ARGUMENT, "bad texture dims");
@@ -1343,7 +1434,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         pp.c = d->channels;
         pp.hm = d->hidden_mats;
         pp.wimg = t->wimg;
-        prep_kernel<<<pp.prep_blocks + (wimg_items(pp.hm) + 255) / 256, 256, 0, st>>>(pp);
+        prep_kernel<<<pp.prep_blocks + (wimg_items(pp.hm, pp.D + 1 > 64 ? 2 : 1) + 255) / 256, 256, 0, st>>>(pp);
         // t1, t3-t7
         TrainParams tp;
         memset(&tp, 0, sizeof tp);
@@ -1398,12 +1489,19 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.P = (int32_t)P;
         if (const char* dbg = getenv("NTC_DEBUG_TRAIN")) tp.debug_flags = atoi(dbg);
         tp.freeze = hp->freeze_latents;
-        const int hm = d->hidden_mats, slots = hm == 1 ? TrainSmemT<1>::SLOTS : TrainSmemT<2>::SLOTS;
-        const uint32_t smem_bytes = hm == 1 ? TrainSmemT<1>::BYTES : TrainSmemT<2>::BYTES;
+        int slots = 1;
+        uint32_t smem_bytes = 0;
+        void (*k)(TrainParams) = nullptr;
+        train_dispatch(d, [&](auto pr, auto a, auto h) {
+            using PP = decltype(pr);
+            constexpr int A = decltype(a)::value, H = decltype(h)::value;
+            using SS = TrainSmemT<H, TrainGeom<PP>::KA>;
+            slots = SS::SLOTS;
+            smem_bytes = SS::BYTES;
+            k = train_kernel<PP, A, H>;
+        });
         const int grid = (int)std::min<int64_t>(std::min<int64_t>(t->num_sms, 8 * RED_MAXK),
                                                 (tiles + slots - 1) / slots);
-        auto* k = hm == 1 ? (d->activation == 1 ? train_kernel<8, 12, 1, 1> : train_kernel<8, 12, 0, 1>)
-                          : (d->activation == 1 ? train_kernel<8, 12, 1, 2> : train_kernel<8, 12, 0, 2>);
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
         if (e == cudaSuccess) {
             k<<<grid, slots * 256, smem_bytes, st>>>(tp);

@@ -17,8 +17,8 @@ DEV = "cuda:0"
 REL = 1e-2
 
 
-def _setup(O, W, c, seed, mip, n_crops, crop, out_gain=1.0, activation=0, hidden_mats=1):
-    d = Profile.named("ntc0.2", W, c, hidden_mats, activation)
+def _setup(O, W, c, seed, mip, n_crops, crop, out_gain=1.0, activation=0, hidden_mats=1, profile="ntc0.2"):
+    d = Profile.named(profile, W, c, hidden_mats, activation)
     lat = gen_latents(seed, O.num_latents(d))
     par = gen_weights_f32(seed + 1, d.input_dim, c, hidden_mats, out_gain=out_gain)
     chain = box_mip_chain_u8(gen_reference_u8(seed + 2, W, c))
@@ -115,6 +115,19 @@ def test_train_grads_depth2(O, mip, n_crops, crop, act):
     d, lat, par, ref, crops = _setup(O, 64, 9, 60 + mip, mip, n_crops, crop, activation=act, hidden_mats=2)
     loss, gp, gl, _ = _gpu_grads(O, d, lat, par, ref, crops, mip, 61, 3)
     loss_o, dp, dl = O.train_grads(d, lat, par, mip, crops, ref, 61, 3)
+    assert abs(loss - loss_o) <= 1e-3 * loss_o
+    _check_all(O, d, gp, gl, dp, dl)
+
+
+@pytest.mark.parametrize("profile,mip,hm,act", [("ntc0.5", 0, 1, 0), ("ntc0.5", 2, 1, 0), ("ntc1.0", 0, 1, 0),
+                                                ("ntc1.0", 3, 1, 1), ("ntc2.25", 0, 1, 0), ("ntc2.25", 1, 2, 0)])
+def test_train_grads_other_profiles(O, profile, mip, hm, act):
+    """f4: the K1 = 80/96 profiles of Table 2 (X in two K atoms, one slot per CTA): loss and
+    every gradient tensor vs the oracle, at several LODs, depths and activations."""
+    d, lat, par, ref, crops = _setup(O, 64, 9, 80 + mip, mip, 2, 24 >> min(mip, 2), activation=act, hidden_mats=hm,
+                                     profile=profile)
+    loss, gp, gl, _ = _gpu_grads(O, d, lat, par, ref, crops, mip, 81, 2)
+    loss_o, dp, dl = O.train_grads(d, lat, par, mip, crops, ref, 81, 2)
     assert abs(loss - loss_o) <= 1e-3 * loss_o
     _check_all(O, d, gp, gl, dp, dl)
 

@@ -23,12 +23,14 @@ def _material(O, d, seed):
     return lat, par, chain
 
 
-@pytest.mark.parametrize("mip,hidden,act", [(0, 1, 0), (1, 1, 0), (4, 1, 0), (0, 2, 0), (0, 1, 1), (1, 2, 1)])
-def test_gradients_finite_difference(O, mip, hidden, act):
+@pytest.mark.parametrize("mip,hidden,act,profile", [(0, 1, 0, "ntc0.2"), (1, 1, 0, "ntc0.2"), (4, 1, 0, "ntc0.2"),
+                                                    (0, 2, 0, "ntc0.2"), (0, 1, 1, "ntc0.2"), (1, 2, 1, "ntc0.2"),
+                                                    (0, 1, 0, "ntc2.25"), (1, 1, 0, "ntc1.0")])
+def test_gradients_finite_difference(O, mip, hidden, act, profile):
     """Analytic gradients vs central differences (exact-input mode, h = 1e-6): per-tensor
     relative L2 error < 1e-4 on sampled weights and every touched latent sample; hardGELU
     (act 0) and exact GELU (act 1, the f4 variant)."""
-    d = Profile.named("ntc0.2", 32, 3, hidden, act)
+    d = Profile.named(profile, 32, 3, hidden, act)
     lat, par, chain = _material(O, d, 100 + mip)
     ref = u8_to_f16_bits(chain[mip])
     crops = gen_crops(5, 32, mip, 2, crop=8)
