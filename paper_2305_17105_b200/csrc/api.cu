@@ -380,6 +380,12 @@ static ntc_status launch_tiles(const ntc_material* m, int mip_first, int mip_cou
     for (int i = mip_count; i <= MAX_MIPS; ++i) p.tile_start[i] = INT32_MAX;
     p.tile_start[mip_count] = (int32_t)t;
     p.n_tiles = (int32_t)t;
+    p.pair_tiles = 0;
+    if ((m->d.channels & 1) && ((uintptr_t)out & 3) == 0)
+        for (int i = 0; i < mip_count; ++i) {
+            if ((m->d.width >> (mip_first + i)) < TILE_M || (out_off[i] & 1) || (row_stride[i] & 1)) break;
+            p.pair_tiles = p.tile_start[i + 1];
+        }
     // part of the tile range: [t*part/nparts, t*(part+1)/nparts)
     const int64_t t0 = t * part / nparts, t1 = t * (part + 1) / nparts;
     p.tile_first = (int32_t)t0;
@@ -429,6 +435,7 @@ cudaError_t ntc::decode_queries(const ntc_material* m, const ntc_query* q, int64
     p.nq = n;
     p.out = out;
     p.status = status;
+    p.pair_tiles = (m->d.channels & 1) && ((uintptr_t)out & 3) == 0 ? (int32_t)(n / TILE_M) : 0;
     return launch_decode(m->pid, m->d.hidden_mats, p, grid_for(m, (n + TILE_M - 1) / TILE_M), s);
 }
 

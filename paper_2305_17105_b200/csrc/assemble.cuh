@@ -65,16 +65,19 @@ __device__ __forceinline__ Cell<BYTES> load_cell(const uint8_t* base, int64_t id
     return c;
 }
 
-// dequantise the two codes held in bits [0,B) and [16,16+B) of `lanes` (already masked):
-// half(0x6400 | code) = 1024 + code; one HFMA2 gives (code - N/2 + 1) / N exactly
-// (R10).
-template <int B>
+// dequantise the two codes held in bits [SH,SH+B) and [16+SH,16+SH+B) of `lanes` (already
+// masked, SH + B <= 10): half(0x6400 | code << SH) = 1024 + code 2^SH; one HFMA2 with the
+// power-of-2 scale Q / 2^SH gives (code - N/2 + 1) / N exactly (R10): the
+// product is exact and the result is representable, so the single rounding is exact.
+template <int B, int SH = 0>
 __device__ __forceinline__ uint32_t dequant2(uint32_t lanes) {
+    static_assert(SH + B <= 10, "code bits must stay inside the fp16 mantissa");
     constexpr float Q = 1.0f / (float)(1 << B);
     constexpr float OFF = (float)((1 << B) / 2 - 1);
+    constexpr float SC = Q / (float)(1 << SH);
     const uint32_t v = lanes | 0x64006400u;
-    __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&v), __float2half2_rn(Q),
-                        __float2half2_rn(-(1024.0f + OFF) * Q));
+    __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&v), __float2half2_rn(SC),
+                        __float2half2_rn(-(1024.0f / (float)(1 << SH) + OFF) * Q));
     return *reinterpret_cast<uint32_t*>(&r);
 }
 
@@ -99,11 +102,17 @@ template <class P>
 struct Fetch {
     Cell<P::CELL0> g0[4];
     Cell<P::CELL1> g1[4];
-    uint32_t wt[4];  // bilinear weights of the G1 taps in units of 1/256 (exact)
-    int m, x, y;
-    bool valid, bad;
+    // packed (one register, it lives across a whole tile): x mod 8 [0,3), y mod 8 [3,6),
+    // mip [6,10), G1 fractional offsets ax [10,15) and ay [15,20) in 1/16 (exact), then the
+    // decode kernel's row flags: valid (bit 20), bad query (bit 21)
+    uint32_t info;
     uint16_t* dst;   // output row of this texel
 };
+__device__ __forceinline__ int info_px(uint32_t i) { return (int)(i & 7u); }
+__device__ __forceinline__ int info_py(uint32_t i) { return (int)((i >> 3) & 7u); }
+__device__ __forceinline__ int info_m(uint32_t i) { return (int)((i >> 6) & 15u); }
+__device__ __forceinline__ uint32_t info_ax(uint32_t i) { return (i >> 10) & 31u; }
+__device__ __forceinline__ uint32_t info_ay(uint32_t i) { return (i >> 15) & 31u; }
 
 // R1/R2/R3: u = (x + 1/2) r / w_m - 1/2 with clamp-to-edge taps (i, j), (i+1, j), (i, j+1),
 // (i+1, j+1).  All sizes are powers of two, so in integers: num = (2x + 1) r - w_m,
@@ -113,9 +122,6 @@ struct Fetch {
 template <class P>
 __device__ __forceinline__ void fetch_texel(const DecodeParams& p, const uint8_t* grids, int m, int x, int y,
                                             Fetch<P>& f, int32_t* dbg_addr) {
-    f.m = m;
-    f.x = x;
-    f.y = y;
     const int j = p.level_of[m];
     const LevelGeom g = p.lv[j];
     const int lw = p.M - 1 - m;  // log2(w_m)
@@ -135,10 +141,7 @@ __device__ __forceinline__ void fetch_texel(const DecodeParams& p, const uint8_t
         const int mask = (2 << lw) - 1;
         const uint32_t ax = (uint32_t)(((nx & mask) << 4) >> (lw + 1));
         const uint32_t ay = (uint32_t)(((ny & mask) << 4) >> (lw + 1));
-        f.wt[0] = (16u - ax) * (16u - ay);
-        f.wt[1] = ax * (16u - ay);
-        f.wt[2] = (16u - ax) * ay;
-        f.wt[3] = ax * ay;
+        f.info = (uint32_t)(x & 7) | ((uint32_t)(y & 7) << 3) | ((uint32_t)m << 6) | (ax << 10) | (ay << 15);
         tx1[0] = max(i, 0);
         tx1[1] = min(i + 1, g.r1 - 1);
         ty1[0] = max(k, 0);
@@ -168,8 +171,10 @@ __device__ __forceinline__ void g0_words_c8b2(const uint32_t (&cell)[4], uint32_
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const uint32_t y = __byte_perm(cell[t], 0u, 0x4140);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) w[4 * t + k] = dequant2<2>((y >> (2 * k)) & 0x00030003u);
+        w[4 * t + 0] = dequant2<2, 0>(y & 0x00030003u);
+        w[4 * t + 1] = dequant2<2, 2>(y & 0x000C000Cu);
+        w[4 * t + 2] = dequant2<2, 4>(y & 0x00300030u);
+        w[4 * t + 3] = dequant2<2, 6>(y & 0x00C000C0u);
     }
 }
 
@@ -294,14 +299,16 @@ __device__ __forceinline__ void assemble_words(const DecodeParams& p, const uint
 #pragma unroll
             for (int wd = 0; wd < NWD; ++wd) cell[t][wd] = f.g1[t].w[wd];
         uint32_t g[P::C1 / 2];
-        g1_words<P, NWD>(cell, f.wt, g);
+        const uint32_t ax = info_ax(f.info), ay = info_ay(f.info);
+        const uint32_t wt[4] = {(16u - ax) * (16u - ay), ax * (16u - ay), (16u - ax) * ay, ax * ay};
+        g1_words<P, NWD>(cell, wt, g);
 #pragma unroll
         for (int k = 0; k < P::C1 / 2; ++k) w[2 * P::C0 + k] = g[k];
     }
     constexpr int PEW = (4 * P::C0 + P::C1) / 2;
     {
         uint32_t pw[7];
-        pe_lod_words(p, s_pe, f.m, f.x, f.y, pw);
+        pe_lod_words(p, s_pe, info_m(f.info), info_px(f.info), info_py(f.info), pw);
 #pragma unroll
         for (int k = 0; k < 7; ++k) w[PEW + k] = pw[k];
     }

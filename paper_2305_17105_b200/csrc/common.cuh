@@ -63,6 +63,10 @@ struct DecodeParams {
     int32_t* dbg_addr;
     uint16_t* dbg_X;
     uint16_t* out;
+    // paired odd-c stores (decode.cu store_output) for tiles < pair_tiles: those tiles' rows
+    // are consecutive output rows starting 4-byte aligned (mode 0: the mips of width >= 128
+    // with even offsets and strides, which come first; mode 1: the full tiles)
+    int32_t pair_tiles;
     float b3[16];                  // output bias, added in the output epilogue
 };
 

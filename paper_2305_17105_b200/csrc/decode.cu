@@ -142,22 +142,42 @@ __device__ __forceinline__ void fetch_tile(const DecodeParams& p, const Run R, i
         }
         f.dst = p.out + qi * p.c;
     }
-    f.valid = valid;
-    f.bad = bad;
     fetch_texel<P>(p, MULTI ? R.grids : p.grids, m, x, y, f, nullptr);
+    f.info |= ((uint32_t)valid << 20) | ((uint32_t)bad << 21);
 }
 
 // a7 store of one texel's c fp16 channels (o = 8 packed pairs).  c is uniform, so the
 // branches below are uniform: even c -> every texel row is 4-byte aligned (b32 pairs),
 // odd c -> b16 stores.
-__device__ __forceinline__ void store_output(const DecodeParams& p, uint16_t* dst, bool valid, bool bad,
-                                             const uint32_t (&o)[8]) {
-    if (!valid) return;
+// pair (uniform per tile, odd c): rows 2i and 2i+1 are one 4-byte-aligned run of 2c halves;
+// the even row's lane writes its (c+1)/2 words, the last one completed with the odd row's
+// first channel (one shuffle), and the odd row's lane writes the remaining (c-1)/2 words.
+__device__ __forceinline__ void store_output(const DecodeParams& p, uint16_t* dst, bool valid, bool bad, bool pair,
+                                             int row, const uint32_t (&o)[8]) {
     uint32_t v[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = bad ? 0x7E007E00u : o[k];  // NaN row for a bad query
-    if (bad && p.status) atomicOr(p.status, (int)NTC_ERR_OUT_OF_RANGE);
+    for (int k = 0; k < 8; ++k) v[k] = o[k];
+    if (p.mode != 0) {  // queries: NaN row for a bad one (uniform branch)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = bad ? 0x7E007E00u : v[k];
+        if (bad && p.status) atomicOr(p.status, (int)NTC_ERR_OUT_OF_RANGE);
+    }
     const int c = p.c;
+    if (pair) {
+        const uint32_t partner = __shfl_xor_sync(0xffffffffu, v[0], 1);
+        const bool odd = row & 1;
+        const uint32_t sel = odd ? 0x5432u : 0x3210u;
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + (odd ? 1 : 0));
+        const int nw = (c - 1) >> 1;
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+            if (k < nw) d32[k] = __byte_perm(v[k], v[k + 1], sel);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k == nw && !odd) d32[k] = __byte_perm(v[k], partner, 0x5410);
+        return;
+    }
+    if (!valid) return;
     if ((c & 1) == 0) {
         uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
 #pragma unroll
@@ -179,7 +199,7 @@ struct Ctx {
     int tile;           // current tile of this context (>= ntiles: idle)
     Fetch<P> nxt;       // prefetched latents of the context's next tile
     uint16_t* dst;      // current texel's output row
-    bool valid, bad;
+    uint32_t flags;     // bit 0 valid, bit 1 bad query
     uint32_t phase;
     uint32_t abuf, tcol;
     uint64_t* bar;
@@ -277,8 +297,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
             store_row<P::K1W>(C.abuf, row, xw);
         }
         C.dst = C.nxt.dst;
-        C.valid = C.nxt.valid;
-        C.bad = C.nxt.bad;
+        C.flags = C.nxt.info >> 20;
         fence_proxy_async_smem();
         tc_fence_before();
         handoff(C);
@@ -330,7 +349,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         for (int k = 0; k < 8; ++k)
             o[k] = pack_half2(__saturatef(__uint_as_float(r[2 * k]) + (MULTI ? R.b3 : p.b3)[2 * k]),
                               __saturatef(__uint_as_float(r[2 * k + 1]) + (MULTI ? R.b3 : p.b3)[2 * k + 1]));
-        store_output(p, C.dst, C.valid, C.bad, o);  // R13: clamp [0,1]
+        store_output(p, C.dst, C.flags & 1, C.flags & 2, !MULTI && C.tile < p.pair_tiles, row, o);  // R13: clamp [0,1]
         tc_fence_before();
         C.tile += stride;
         phase0(C);

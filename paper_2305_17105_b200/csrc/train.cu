@@ -124,7 +124,7 @@ struct TrainSmemT {
     };
     static constexpr int SLOTS = (HM == 1 && KA == 1) ? 2 : 1;
     static constexpr uint32_t WG_BYTES = NT * TILE;
-    static constexpr uint32_t MISC = 256 + 16 * NTC_MAX_CROPS + 4 * (NTC_MAX_CROPS + 1) + 12;
+    static constexpr uint32_t MISC = 256 + 16 * NTC_MAX_CROPS + 4 * (NTC_MAX_CROPS + 1) + 4 * NTC_MAX_CROPS + 12;
     static constexpr uint32_t BYTES = 1024 + WEND + SLOTS * WG_BYTES + MISC;
 };
 using TrainSmem = TrainSmemT<1>;
@@ -254,6 +254,18 @@ __device__ __forceinline__ void act_and_grad(float z, float& h, float& g) {
     }
 }
 
+// hardGELU and its derivative (R15) of a column pair, as packed fp16 words.  Outside the
+// middle piece s = sat(z/3 + 1/2) is exactly the derivative (0 below -3/2, 1 above +3/2), so
+// g = |z| <= 3/2 ? 2z/3 + 1/2 : s (equal to hgelu_d for every finite z); h and t run packed.
+__device__ __forceinline__ void hgelu_and_grad2(float z0, float z1, uint32_t& hw, uint32_t& gw) {
+    const float2 z = make_float2(z0, z1);
+    const float2 s = make_float2(__saturatef(fmaf(z0, 1.0f / 3.0f, 0.5f)), __saturatef(fmaf(z1, 1.0f / 3.0f, 0.5f)));
+    const float2 hh = __fmul2_rn(z, s);
+    const float2 t = __ffma2_rn(z, make_float2(2.0f / 3.0f, 2.0f / 3.0f), make_float2(0.5f, 0.5f));
+    hw = pack_half2(hh.x, hh.y);
+    gw = pack_half2(fabsf(z0) <= 1.5f ? t.x : s.x, fabsf(z1) <= 1.5f ? t.y : s.y);
+}
+
 template <class P> struct TrainGeom {
     static constexpr int C0 = P::C0, C1 = P::C1;
     static constexpr int D = 4 * C0 + C1 + 13, NLAT = 4 * C0 + C1;
@@ -286,6 +298,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     uint32_t* s_tmem = s_pe + 32;
     int4* s_crop = reinterpret_cast<int4*>(s_tmem + 4);
     int* s_ts = reinterpret_cast<int*>(s_crop + NTC_MAX_CROPS);
+    int* s_csh = s_ts + NTC_MAX_CROPS + 1;  // log2 of the crop width when it is a power of 2, else -1
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int slot = warp >> 3, h = (warp >> 2) & 1, q = warp & 3, row = q * 32 + lane;
@@ -297,7 +310,11 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.wimg) + i);
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
     if (tid < 4) s_loss[tid] = 0.0f;
-    if (tid < NTC_MAX_CROPS) s_crop[tid] = make_int4(p.crop[tid][0], p.crop[tid][1], p.crop[tid][2], p.crop[tid][3]);
+    if (tid < NTC_MAX_CROPS) {
+        s_crop[tid] = make_int4(p.crop[tid][0], p.crop[tid][1], p.crop[tid][2], p.crop[tid][3]);
+        const int cw = p.crop[tid][2];
+        s_csh[tid] = cw > 0 && (cw & (cw - 1)) == 0 ? __ffs(cw) - 1 : -1;
+    }
     if (tid <= NTC_MAX_CROPS) s_ts[tid] = p.tile_start[tid];
     if (tid == 0) {
         for (int i = 0; i < 2 * SLOTS; ++i) mbar_init(&s_bar[i], 1);
@@ -375,8 +392,17 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         const int li = (tile - s_ts[k]) * TILE_M + row;
         Texel t;
         t.valid = li < cr.z * cr.w;
-        t.x = cr.x + (t.valid ? li % cr.z : 0);
-        t.y = cr.y + (t.valid ? li / cr.z : 0);
+        const int sh = s_csh[k];  // uniform per tile: power-of-2 crops (the paper's 256^2) shift
+        int qx, qy;
+        if (sh >= 0) {
+            qx = li & (cr.z - 1);
+            qy = li >> sh;
+        } else {
+            qy = li / cr.z;
+            qx = li - qy * cr.z;
+        }
+        t.x = cr.x + (t.valid ? qx : 0);
+        t.y = cr.y + (t.valid ? qy : 0);
         return t;
     };
     // G0 taps (half 0) / G1 taps and bilinear weights in 1/256 units (half 1)
@@ -542,15 +568,20 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             for (int i = 0; i < 16; ++i) {
                 float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
                 if (bias) {
-                    const float2 bb = *reinterpret_cast<const float2*>(bias + 32 * h + 2 * i);
-                    z0 += bb.x;
-                    z1 += bb.y;
+                    const float2 zb = __fadd2_rn(make_float2(z0, z1),
+                                                 *reinterpret_cast<const float2*>(bias + 32 * h + 2 * i));
+                    z0 = zb.x;
+                    z1 = zb.y;
                 }
-                float h0, h1, g0, g1;
-                act_and_grad<ACT>(z0, h0, g0);
-                act_and_grad<ACT>(z1, h1, g1);
-                hv[i] = h2u(h0, h1);
-                gv[i] = h2u(g0, g1);
+                if constexpr (ACT == 0) {
+                    hgelu_and_grad2(z0, z1, hv[i], gv[i]);
+                } else {
+                    float h0, h1, g0, g1;
+                    act_and_grad<ACT>(z0, h0, g0);
+                    act_and_grad<ACT>(z1, h1, g1);
+                    hv[i] = h2u(h0, h1);
+                    gv[i] = h2u(g0, g1);
+                }
             }
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {

@@ -167,6 +167,51 @@ def test_decode_texels_random_and_errors(O):
     ntc.ntc_decode_texels(mat, empty, torch.empty((0, 16), dtype=torch.float16, device=DEV))
 
 
+@pytest.mark.parametrize("c,off", [(1, 2), (3, 2), (7, 2), (9, 2), (15, 2), (9, 1)])
+def test_decode_texels_odd_channels_paired_stores(O, c, off):
+    """Odd c: full tiles take the paired-row store path (the even row's lane completes its
+    last word with the odd row's first channel).  Bad queries on even and odd rows inside
+    full tiles, a ragged tail, and the output's neighbours left untouched."""
+    d = Profile.named("ntc0.2", 256, c)
+    mat, codes, w = _material(O, d, 0x4E5400 + c)
+    allq = gen_queries(11 + c, 256, 128 * 5 + 77, "area")
+    bad_rows = [130, 131, 256 + 7, 384 + 64]
+    allq[bad_rows] = np.array([[256, 0, 0], [0, 0, 9], [0, 200, 1], [5, 5, 30]], np.int32)
+    n = allq.shape[0]
+    q = ntc.pack_queries(torch.from_numpy(allq).to(DEV))
+    buf = torch.full((n + 4, c), -1.0, dtype=torch.float16, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ntc.ntc_decode_texels(mat, q, buf[off:n + off], st)  # off = 1: 2-byte-aligned output (fallback)
+    torch.cuda.synchronize()
+    got = buf.float().cpu().numpy()
+    assert np.all(got[:off] == -1.0) and np.all(got[n + off:] == -1.0)
+    got = got[off:n + off]
+    assert int(st.item()) & ntc.NTC_ERR_OUT_OF_RANGE
+    ok = np.ones(n, bool)
+    ok[bad_rows] = False
+    assert np.all(np.isnan(got[~ok]))
+    ref = O.decode_texels(d, codes, w, allq[ok])
+    assert np.abs(got[ok] - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("stride_pad", [0, 1, 2])
+def test_decode_mip_odd_channels_strides(O, stride_pad):
+    """decode_mip of a 256-wide mip with odd c: even strides use the paired stores, an odd
+    stride (or odd base offset) falls back to per-channel stores; padding stays untouched."""
+    c = 7
+    d = Profile.named("ntc0.2", 256, c)
+    mat, codes, w = _material(O, d, 9)
+    rs = 256 * c + stride_pad
+    buf = torch.full((256 * rs + 1,), -1.0, dtype=torch.float16, device=DEV)
+    view = buf[1:] if stride_pad == 2 else buf[:-1]  # odd base offset in one case
+    ntc.ntc_decode_mip(mat, 0, view, row_stride_elems=rs)
+    torch.cuda.synchronize()
+    got = view.float().cpu().numpy().reshape(256, rs)
+    assert np.all(got[:, 256 * c:] == -1.0)
+    err = np.abs(got[:, :256 * c].reshape(256, 256, c) - O.decode_mip(d, codes, w, 0))
+    assert err.max() <= TOL
+
+
 def test_invalid_arguments(O):
     d = Profile.named("ntc0.2", 64, 8)
     mat, _, _ = _material(O, d, 1)

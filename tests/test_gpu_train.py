@@ -86,7 +86,7 @@ def _check_all(O, d, gp, gl, dp, dl):
                 assert np.all(gl[a:b] == 0)
 
 
-@pytest.mark.parametrize("mip,n_crops,crop", [(0, 2, 32), (1, 3, 16), (2, 4, 8), (4, 1, 4), (5, 2, 2)])
+@pytest.mark.parametrize("mip,n_crops,crop", [(0, 2, 32), (1, 3, 16), (2, 4, 8), (4, 1, 4), (5, 2, 2), (0, 3, 24), (1, 2, 20)])
 def test_train_grads_small(O, mip, n_crops, crop):
     """Loss and every gradient tensor vs the oracle on a 64^2 x 8 material, at several LODs
     (crops smaller than a tile, ragged last tiles, overlapping crops)."""
