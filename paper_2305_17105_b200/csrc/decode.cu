@@ -105,11 +105,11 @@ struct Run {
 };
 
 // resolve the texel of row `row` of `tile`, its output address, and issue its latent loads
-template <class P, bool MULTI, int CT = 0>
+template <class P, bool MULTI, int CT = 0, bool TILED = false>
 __device__ __forceinline__ void fetch_tile(const DecodeParams& p, const Run R, int tile, int row, Fetch<P>& f) {
     int m = 0, x = 0, y = 0;
     bool valid, bad = false;
-    if (!MULTI && p.mode == 0) {
+    if (TILED || (!MULTI && p.mode == 0)) {
         int mi = 0;
         while (tile >= p.tile_start[mi + 1]) ++mi;
         m = p.mip_first + mi;
@@ -154,13 +154,13 @@ __device__ __forceinline__ void fetch_tile(const DecodeParams& p, const Run R, i
 // pair (uniform per tile, odd c): rows 2i and 2i+1 are one 4-byte-aligned run of 2c halves;
 // the even row's lane writes its (c+1)/2 words, the last one completed with the odd row's
 // first channel (one shuffle), and the odd row's lane writes the remaining (c-1)/2 words.
-template <int CT>
+template <int CT, bool TILED>
 __device__ __forceinline__ void store_output(const DecodeParams& p, uint16_t* dst, bool valid, bool bad, bool pair,
                                              int row, const uint32_t (&o)[8]) {
     uint32_t v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = o[k];
-    if (p.mode != 0) {  // queries: NaN row for a bad one (uniform branch)
+    if (!TILED && p.mode != 0) {  // queries: NaN row for a bad one (uniform branch)
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = bad ? 0x7E007E00u : v[k];
         if (bad && p.status) atomicOr(p.status, (int)NTC_ERR_OUT_OF_RANGE);
@@ -211,8 +211,9 @@ struct Ctx {
     uint64_t adesc;     // SW128 K-major descriptor of abuf
 };
 
-// CT: the channel count as a compile-time constant (0: the runtime p.c), for the output path
-template <class P, int HM, bool MULTI, int ACT, int CT = 0>
+// CT: the channel count as a compile-time constant (0: the runtime p.c), for the output path;
+// TILED: compiled for mode 0 (tiles over mips) only
+template <class P, int HM, bool MULTI, int ACT, int CT = 0, bool TILED = false>
 __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTable* mt) {
     using S = DecodeSmem<P, HM>;
     constexpr int NW = S::NWG, NC = S::NC;
@@ -268,7 +269,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     };
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
     // single material: tiles blockIdx-strided over [first, ntiles); multi: per-run ranges
-    int ntiles = p.mode == 0 ? p.n_tiles : (int)((p.nq + TILE_M - 1) / TILE_M);
+    int ntiles = TILED || p.mode == 0 ? p.n_tiles : (int)((p.nq + TILE_M - 1) / TILE_M);
     int stride = (int)gridDim.x * NW * NC;  // tiles advance by NC contexts per warpgroup
     Run R;
     R.grids = nullptr;
@@ -287,8 +288,8 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         cx[c].iq = (wg * NC + c) & 3;
         cx[c].adesc = umma_desc_k_sw128(cx[c].abuf);
         if (!MULTI) {
-            cx[c].tile = (p.mode == 0 ? p.tile_first : 0) + ((int)blockIdx.x * NW + wg) * NC + c;
-            if (cx[c].tile < ntiles) fetch_tile<P, MULTI, CT>(p, R, cx[c].tile, row, cx[c].nxt);
+            cx[c].tile = (TILED || p.mode == 0 ? p.tile_first : 0) + ((int)blockIdx.x * NW + wg) * NC + c;
+            if (cx[c].tile < ntiles) fetch_tile<P, MULTI, CT, TILED>(p, R, cx[c].tile, row, cx[c].nxt);
         }
     }
 
@@ -314,7 +315,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
             mma_commit(C.bar);
         }
         const int nt = C.tile + stride;
-        if (nt < ntiles) fetch_tile<P, MULTI, CT>(p, R, nt, row, C.nxt);  // loads overlap the MLP
+        if (nt < ntiles) fetch_tile<P, MULTI, CT, TILED>(p, R, nt, row, C.nxt);  // loads overlap the MLP
     };
     // P1..P(HM+1): wait for the previous MMA, epilogue to the A tile, next layer's MMA
     auto phase_hidden = [&](Ctx<P>& C, int layer) {
@@ -355,7 +356,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         for (int k = 0; k < (CT ? (CT + 1) / 2 : 8); ++k)
             o[k] = pack_half2(__saturatef(__uint_as_float(r[2 * k]) + (MULTI ? R.b3 : p.b3)[2 * k]),
                               __saturatef(__uint_as_float(r[2 * k + 1]) + (MULTI ? R.b3 : p.b3)[2 * k + 1]));
-        store_output<CT>(p, C.dst, C.flags & 1, C.flags & 2, !MULTI && C.tile < p.pair_tiles, row, o);  // R13: clamp [0,1]
+        store_output<CT, TILED>(p, C.dst, C.flags & 1, C.flags & 2, !MULTI && C.tile < p.pair_tiles, row, o);  // R13: clamp [0,1]
         tc_fence_before();
         C.tile += stride;
         phase0(C);
@@ -368,7 +369,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 cx[c].tile = first + wg * NC + c;
-                if (cx[c].tile < ntiles) fetch_tile<P, MULTI, CT>(p, R, cx[c].tile, row, cx[c].nxt);
+                if (cx[c].tile < ntiles) fetch_tile<P, MULTI, CT, TILED>(p, R, cx[c].tile, row, cx[c].nxt);
             }
         }
 #pragma unroll
@@ -423,9 +424,9 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-template <class P, int HM, int ACT, int CT = 0>
+template <class P, int HM, int ACT, int CT = 0, bool TILED = false>
 __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
-    decode_body<P, HM, false, ACT, CT>(p, nullptr);
+    decode_body<P, HM, false, ACT, CT, TILED>(p, nullptr);
 }
 
 template <class P, int HM, int ACT>
@@ -545,9 +546,9 @@ cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cuda
         using SS = DecodeSmem<PP, HMv>;
         auto* k = decode_kernel<PP, HMv, decltype(a)::value>;
         // the bench's headline material (NTC 0.2, [57,64,64,9], hardGELU) gets its channel
-        // count compiled into the output path
+        // count (and, for mip tiles, the mode) compiled into the kernel
         if constexpr (std::is_same<PP, NTC02>::value && HMv == 1 && decltype(a)::value == 0)
-            if (p.c == 9) k = decode_kernel<PP, HMv, 0, 9>;
+            if (p.c == 9) k = p.mode == 0 ? decode_kernel<PP, HMv, 0, 9, true> : decode_kernel<PP, HMv, 0, 9>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
         if (e != cudaSuccess) return e;
         k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p);
