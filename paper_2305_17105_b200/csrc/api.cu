@@ -380,6 +380,14 @@ static ntc_status launch_tiles(const ntc_material* m, int mip_first, int mip_cou
     for (int i = mip_count; i <= MAX_MIPS; ++i) p.tile_start[i] = INT32_MAX;
     p.tile_start[mip_count] = (int32_t)t;
     p.n_tiles = (int32_t)t;
+    p.lin_tiles = 0;
+    for (int i = 0; i < mip_count; ++i) {
+        const int64_t w = m->d.width >> (mip_first + i);
+        if ((w * w) % TILE_M || out_off[i] != (int64_t)p.tile_start[i] * TILE_M * m->d.channels ||
+            row_stride[i] != w * m->d.channels)
+            break;
+        p.lin_tiles = p.tile_start[i + 1];
+    }
     p.pair_tiles = 0;
     if ((m->d.channels & 1) && ((uintptr_t)out & 3) == 0)
         for (int i = 0; i < mip_count; ++i) {

@@ -67,6 +67,9 @@ struct DecodeParams {
     // are consecutive output rows starting 4-byte aligned (mode 0: the mips of width >= 128
     // with even offsets and strides, which come first; mode 1: the full tiles)
     int32_t pair_tiles;
+    // mode 0: tiles < lin_tiles write output row (tile * 128 + row) of `out` (whole-tile mips
+    // laid out back to back from out_off 0, rows of w_m * c elements)
+    int32_t lin_tiles;
     float b3[16];                  // output bias, added in the output epilogue
 };
 

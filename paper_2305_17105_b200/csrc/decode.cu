@@ -111,7 +111,8 @@ __device__ __forceinline__ void fetch_tile(const DecodeParams& p, const Run R, i
     bool valid, bad = false;
     if (TILED || (!MULTI && p.mode == 0)) {
         int mi = 0;
-        while (tile >= p.tile_start[mi + 1]) ++mi;
+        if (tile >= p.tile_start[1])  // most tiles belong to the first mip
+            while (tile >= p.tile_start[mi + 1]) ++mi;
         m = p.mip_first + mi;
         const int local = (tile - p.tile_start[mi]) * TILE_M + row;
         const int lw = p.M - 1 - m;  // log2(w_m)
@@ -120,7 +121,10 @@ __device__ __forceinline__ void fetch_tile(const DecodeParams& p, const Run R, i
             x = local & ((1 << lw) - 1);
             y = local >> lw;
         }
-        f.dst = p.out + (p.out_off[mi] + (int64_t)y * p.row_stride[mi] + x * (CT ? CT : p.c));
+        if (tile < p.lin_tiles)  // uniform: the output row is texel tile * 128 + row of `out`
+            f.dst = p.out + (int64_t)(tile * TILE_M + row) * (CT ? CT : p.c);
+        else
+            f.dst = p.out + (p.out_off[mi] + (int64_t)y * p.row_stride[mi] + x * (CT ? CT : p.c));
     } else {
         int64_t qi;
         if (MULTI) {
