@@ -93,6 +93,35 @@ struct PrepParams {
     uint8_t* wimg;
 };
 
+// Latents per thread of the footprint-box kernels (prep, latent Adam): consecutive flat
+// indices are mostly consecutive latents of one box row, so one box lookup (and, for the
+// noise, one Philox block per 4 latents, R16) serves several latents.
+constexpr int LPT = 4;
+
+// flat index -> box, latent index, position in the box row and the row length
+__device__ __forceinline__ void box_locate_row(const Box* box, const int32_t* start, int nbox, int32_t i, int& b,
+                                               int64_t& li, int32_t& rem, int32_t& w) {
+    b = 0;
+    while (b + 1 < nbox && i >= start[b + 1]) ++b;
+    const Box& B = box[b];
+    const int32_t k = i - start[b];
+    w = (B.x1 - B.x0 + 1) * B.C;
+    const int32_t yy = B.y0 + k / w;
+    rem = k % w;
+    li = B.off + ((int64_t)yy * B.r + B.x0) * B.C + rem;
+}
+
+// advance a box cursor from flat index i - 1 to i
+__device__ __forceinline__ void box_next(const Box* box, const int32_t* start, int nbox, int32_t i, int& b,
+                                         int64_t& li, int32_t& rem, int32_t& w) {
+    if (rem + 1 < w && i < start[b + 1]) {
+        ++li;
+        ++rem;
+    } else {
+        box_locate_row(box, start, nbox, i, b, li, rem, w);
+    }
+}
+
 __device__ __forceinline__ void box_locate(const Box* box, const int32_t* start, int nbox, int32_t i, int& b,
                                            int64_t& li) {
     b = 0;
@@ -220,23 +249,49 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
         }
         return;
     }
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.box_start[p.nbox]) return;
+    const int32_t n = p.box_start[p.nbox];
+    int32_t i = LPT * (int32_t)(blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= n) return;
     int b;
     int64_t li;
-    box_locate(p.box, p.box_start, p.nbox, i, b, li);
-    float v = p.latents[li];
-    if (p.noise_on) {
-        const uint4 r = philox4x32_10(make_uint4((uint32_t)((uint64_t)li >> 2), (uint32_t)((uint64_t)li >> 34), p.step,
-                                                 0x4E4F4953u),
-                                      make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32)));
-        const uint32_t w = (li & 3) == 0 ? r.x : (li & 3) == 1 ? r.y : (li & 3) == 2 ? r.z : r.w;
-        // u = (2 (w >> 9) + 1) 2^-24 in (0, 1); noise = (u - 1/2) Q, exact in fp32
-        const float u = (float)(2u * (w >> 9) + 1u) * 5.9604644775390625e-8f;
-        v += (u - 0.5f) * (1.0f / (float)(1 << p.box[b].bits));
+    int32_t rem, rw;
+    box_locate_row(p.box, p.box_start, p.nbox, i, b, li, rem, rw);
+    // all addresses and loads first (the stores below may alias the latents as far as the
+    // compiler knows), then the noise and the stores
+    int64_t lis[LPT];
+    int bs[LPT];
+    float vs[LPT];
+    const int ne = min(LPT, n - i);
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+        if (e > 0 && e < ne) box_next(p.box, p.box_start, p.nbox, i + e, b, li, rem, rw);
+        lis[e] = li;
+        bs[e] = b;
+        vs[e] = e < ne ? __ldg(p.latents + li) : 0.0f;
     }
-    p.noisy[li] = __float2half_rn(v);
-    p.grad_lat[li] = 0.0f;
+    int64_t ctr = -1;
+    uint4 r = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+        if (e >= ne) break;
+        li = lis[e];
+        b = bs[e];
+        float v = vs[e];
+        if (p.noise_on) {
+            if ((li >> 2) != ctr) {  // Philox block of latents 4k .. 4k+3 (R16)
+                ctr = li >> 2;
+                r = philox4x32_10(make_uint4((uint32_t)((uint64_t)li >> 2), (uint32_t)((uint64_t)li >> 34), p.step,
+                                             0x4E4F4953u),
+                                  make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32)));
+            }
+            const uint32_t w = (li & 3) == 0 ? r.x : (li & 3) == 1 ? r.y : (li & 3) == 2 ? r.z : r.w;
+            // u = (2 (w >> 9) + 1) 2^-24 in (0, 1); noise = (u - 1/2) Q, exact in fp32
+            const float u = (float)(2u * (w >> 9) + 1u) * 5.9604644775390625e-8f;
+            v += (u - 0.5f) * (1.0f / (float)(1 << p.box[b].bits));
+        }
+        p.noisy[li] = __float2half_rn(v);
+        p.grad_lat[li] = 0.0f;
+    }
 }
 
 // hidden activation and its derivative: hardGELU (R15) or exact GELU (f4):
@@ -1079,24 +1134,9 @@ __global__ void __launch_bounds__(256) reduce_adam_kernel(const __grid_constant_
     adam_latent(a, (int64_t)(blockIdx.x - rblocks) * blockDim.x + threadIdx.x);
 }
 
-__device__ void adam_latent(const AdamParams& a, int64_t j) {
-    if (a.freeze) return;
-    int64_t li;
-    int bits;
-    if (a.dense_latents) {
-        if (j >= a.n_latents) return;
-        li = j;
-        int g = 0;
-        while (li >= a.grid_start[g + 1]) ++g;
-        bits = a.grid_bits[g];
-    } else {
-        if (j >= a.box_start[a.nbox]) return;
-        int b;
-        box_locate(a.box, a.box_start, a.nbox, (int32_t)j, b, li);
-        bits = a.box[b].bits;
-    }
+__device__ __forceinline__ void adam_latent_one(const AdamParams& a, int64_t li, int bits, bool sparse) {
     const float g = a.grad_lat[li];
-    if (!a.dense_latents && g == 0.0f) return;  // R18: footprint-sparse Adam skips g == 0
+    if (sparse && g == 0.0f) return;  // R18: footprint-sparse Adam skips g == 0
     float p = a.latents[li], m = a.m_lat[li], v = a.v_lat[li];
     adam_one(p, m, v, g, a.lr_l, a);
     const float N = (float)(1 << bits);
@@ -1104,6 +1144,56 @@ __device__ void adam_latent(const AdamParams& a, int64_t j) {
     a.latents[li] = p;
     a.m_lat[li] = m;
     a.v_lat[li] = v;
+}
+
+// latents LPT j .. LPT j + LPT - 1 of the update set (footprint boxes, or every latent)
+__device__ void adam_latent(const AdamParams& a, int64_t j) {
+    if (a.freeze) return;
+    if (a.dense_latents) {
+#pragma unroll
+        for (int e = 0; e < LPT; ++e) {
+            const int64_t li = LPT * j + e;
+            if (li >= a.n_latents) return;
+            int g = 0;
+            while (li >= a.grid_start[g + 1]) ++g;
+            adam_latent_one(a, li, a.grid_bits[g], false);
+        }
+        return;
+    }
+    const int32_t n = a.box_start[a.nbox];
+    const int32_t i = (int32_t)(LPT * j);
+    if (i >= n) return;
+    int b;
+    int64_t li;
+    int32_t rem, rw;
+    box_locate_row(a.box, a.box_start, a.nbox, i, b, li, rem, rw);
+    // addresses and every load first (the stores may alias them as far as the compiler
+    // knows), then the updates
+    const int ne = min(LPT, n - i);
+    int64_t lis[LPT];
+    int bits[LPT];
+    float g[LPT], pv[LPT], mv[LPT], vv[LPT];
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+        if (e > 0 && e < ne) box_next(a.box, a.box_start, a.nbox, i + e, b, li, rem, rw);
+        lis[e] = li;
+        bits[e] = a.box[b].bits;
+        g[e] = e < ne ? a.grad_lat[li] : 0.0f;
+        pv[e] = e < ne ? a.latents[li] : 0.0f;
+        mv[e] = e < ne ? a.m_lat[li] : 0.0f;
+        vv[e] = e < ne ? a.v_lat[li] : 0.0f;
+    }
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+        if (e >= ne || g[e] == 0.0f) continue;  // R18: footprint-sparse Adam skips g == 0
+        float pe = pv[e], me = mv[e], ve = vv[e];
+        adam_one(pe, me, ve, g[e], a.lr_l, a);
+        const float N = (float)(1 << bits[e]);
+        pe = fminf(fmaxf(pe, -(N - 1.0f) / (2.0f * N)), 0.5f);  // clamp
+        a.latents[lis[e]] = pe;
+        a.m_lat[lis[e]] = me;
+        a.v_lat[lis[e]] = ve;
+    }
 }
 
 }  // namespace ntc
@@ -1459,7 +1549,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         pp.step = (uint32_t)hp->step;
         pp.noise_on = hp->noise_on;
         if (hp->dense_latent_adam) cudaMemsetAsync(buf->grad_lat, 0, sizeof(float) * NL, st);
-        pp.prep_blocks = (n + 255) / 256;
+        pp.prep_blocks = (int32_t)((n + 256 * LPT - 1) / (256 * LPT));
         pp.params = buf->params;
         pp.D = 4 * d->c0 + d->c1 + 13;
         pp.c = d->channels;
@@ -1548,7 +1638,8 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
             if ((flags & NTC_STEP_APPLY) && apply_buffers_ok(buf)) {
                 AdamParams a;
                 const int64_t nlat = build_adam(d, buf, boxes, hp, a);
-                reduce_adam_kernel<<<rblocks + (int)((nlat + 255) / 256), 256, 0, st>>>(ra, a, rblocks);
+                reduce_adam_kernel<<<rblocks + (int)((nlat + 256 * LPT - 1) / (256 * LPT)), 256, 0, st>>>(ra, a,
+                                                                                                    rblocks);
                 e = cudaGetLastError();
                 if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
                 return NTC_OK;
@@ -1615,7 +1706,7 @@ static ntc_status apply_step(const ntc_desc* d, const ntc_train_buffers* buf, co
                              const ntc_train_hparams* hp, cudaStream_t st) {
     if (!apply_buffers_ok(buf)) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
     AdamParams a;
-    const int64_t total = ntc_num_params(d) + build_adam(d, buf, boxes, hp, a);
+    const int64_t total = ntc_num_params(d) + (build_adam(d, buf, boxes, hp, a) + LPT - 1) / LPT;
     adam_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? NTC_OK : api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
