@@ -153,8 +153,8 @@ __device__ __forceinline__ void fetch_tile(const DecodeParams& p, const Run R, i
 }
 
 // a7 store of one texel's c fp16 channels (o = 8 packed pairs).  c is uniform, so the
-// branches below are uniform: even c -> every texel row is 4-byte aligned (b32 pairs),
-// odd c -> b16 stores.
+// branches below are uniform: even c with a 4-byte-aligned output -> b32 pairs (16-byte
+// vectors for the compiled c = 16), otherwise b16 stores.
 // pair (uniform per tile, odd c): rows 2i and 2i+1 are one 4-byte-aligned run of 2c halves;
 // the even row's lane writes its (c+1)/2 words, the last one completed with the odd row's
 // first channel (one shuffle), and the odd row's lane writes the remaining (c-1)/2 words.
@@ -185,7 +185,15 @@ __device__ __forceinline__ void store_output(const DecodeParams& p, uint16_t* ds
         return;
     }
     if (!valid) return;
-    if ((c & 1) == 0) {
+    if constexpr (CT > 0 && CT % 8 == 0) {  // 16-byte rows: vector stores when aligned
+        if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+#pragma unroll
+            for (int k = 0; k < CT / 8; ++k)
+                reinterpret_cast<uint4*>(dst)[k] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            return;
+        }
+    }
+    if ((c & 1) == 0 && (reinterpret_cast<uintptr_t>(dst) & 3u) == 0) {
         uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
@@ -553,6 +561,9 @@ cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cuda
         // count (and, for mip tiles, the mode) compiled into the kernel
         if constexpr (std::is_same<PP, NTC02>::value && HMv == 1 && decltype(a)::value == 0)
             if (p.c == 9) k = p.mode == 0 ? decode_kernel<PP, HMv, 0, 9, true> : decode_kernel<PP, HMv, 0, 9>;
+        // and the 16-channel material of the random-access line (configs[2])
+        if constexpr (std::is_same<PP, NTC02>::value && HMv == 1 && decltype(a)::value == 0)
+            if (p.c == 16) k = p.mode == 0 ? decode_kernel<PP, HMv, 0, 16, true> : decode_kernel<PP, HMv, 0, 16>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
         if (e != cudaSuccess) return e;
         k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p);

@@ -318,3 +318,21 @@ def test_bench_configs_sampled(O):
     sel = rng.choice(n, 150000, replace=False)
     got = out[torch.from_numpy(sel).to(DEV)].float().cpu().numpy()
     assert np.abs(got - O.decode_texels(d, codes, w, xym[sel])).max() <= TOL
+
+
+@pytest.mark.parametrize("off", [0, 1, 8])
+def test_decode_texels_c16_alignment(O, off):
+    """c = 16 (the random-access line's compiled instantiation): 16-byte vector stores when the
+    output rows are 16-byte aligned, per-word stores otherwise; neighbours left untouched."""
+    d = Profile.named("ntc0.2", 256, 16)
+    mat, codes, w = _material(O, d, 0x4E5416)
+    allq = gen_queries(31, 256, 128 * 3 + 50, "area")
+    n = allq.shape[0]
+    q = ntc.pack_queries(torch.from_numpy(allq).to(DEV))
+    buf = torch.full((n * 16 + 32,), -1.0, dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_texels(mat, q, buf[off:off + n * 16])
+    torch.cuda.synchronize()
+    got = buf.float().cpu().numpy()
+    assert np.all(got[:off] == -1.0) and np.all(got[off + n * 16:] == -1.0)
+    ref = O.decode_texels(d, codes, w, allq)
+    assert np.abs(got[off:off + n * 16].reshape(n, 16) - ref).max() <= TOL
