@@ -441,10 +441,10 @@ __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1) decode_kernel
     decode_body<P, HM, false, ACT, CT, TILED>(p, nullptr);
 }
 
-template <class P, int HM, int ACT>
+template <class P, int HM, int ACT, int CT = 0>
 __global__ void __launch_bounds__(DecodeSmem<P, HM>::NWG * 128, 1)
     decode_multi_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ MultiTable mt) {
-    decode_body<P, HM, true, ACT>(p, &mt);
+    decode_body<P, HM, true, ACT, CT>(p, &mt);
 }
 
 // Tests only: the same addressing + assembly, written to global memory in canonical order.
@@ -578,6 +578,9 @@ cudaError_t launch_decode_multi(int pid, int hm, const DecodeParams& p, const Mu
         constexpr int HMv = decltype(h)::value;
         using SS = DecodeSmem<PP, HMv>;
         auto* k = decode_multi_kernel<PP, HMv, decltype(a)::value>;
+        // the 8-channel materials of the multi-material line (Table 4 analog)
+        if constexpr (std::is_same<PP, NTC02>::value && HMv == 1 && decltype(a)::value == 0)
+            if (p.c == 8) k = decode_multi_kernel<PP, HMv, 0, 8>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
         if (e != cudaSuccess) return e;
         k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p, mt);
