@@ -97,6 +97,26 @@ __device__ __forceinline__ void nib_lanes(uint32_t w, uint32_t* out) {
     }
 }
 
+// G1 variant: lane pairs with the code at bit 0 or bit 4 of each 16-bit lane (scale 1 or 16;
+// G1 sums stay below 2^16 either way: 16 * 15 * 256 = 61440), which saves the shifts
+template <int NCH>
+__device__ __forceinline__ void nib_lanes_g1(uint32_t w, uint32_t* out) {
+    if constexpr (NCH == 8) {
+        const uint32_t h = w >> 8;
+        out[0] = w & 0x000F000Fu;  // (0, 4) x1
+        out[1] = w & 0x00F000F0u;  // (1, 5) x16
+        out[2] = h & 0x000F000Fu;  // (2, 6) x1
+        out[3] = h & 0x00F000F0u;  // (3, 7) x16
+    } else if constexpr (NCH == 4) {
+        const uint32_t y = __byte_perm(w, 0u, 0x4140);  // [b0, 0, b1, 0]
+        out[0] = y & 0x000F000Fu;                        // (0, 2) x1
+        out[1] = y & 0x00F000F0u;                        // (1, 3) x16
+    } else {
+        const uint32_t y = w | (w << 12);
+        out[0] = y & 0x000F000Fu;                        // (0, 1) x1
+    }
+}
+
 // ------------------------------------------------------------------ fetch (a1 + loads)
 template <class P>
 struct Fetch {
@@ -193,36 +213,39 @@ __device__ __forceinline__ void g1_words(const uint32_t (&cell)[4][NWD], const u
         uint32_t l[NL];
         int cb[NL];  // first channel of each lane pair, second = cb + step
         int st[NL];
+        float sc[NL];  // lane scale: the code sits at bit 0 (1) or bit 4 (16) of its lane
         int n = 0;
 #pragma unroll
         for (int wd = 0; wd * 8 < P::C1; ++wd) {
             const int nch = P::C1 - wd * 8 >= 8 ? 8 : P::C1 - wd * 8;
             if (nch == 8) {
-                nib_lanes<8>(cell[t][wd], l + n);
+                nib_lanes_g1<8>(cell[t][wd], l + n);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 4; }
+                for (int q = 0; q < 4; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 4; sc[n + q] = (q & 1) ? 16.0f : 1.0f; }
                 n += 4;
             } else if (nch == 4) {
-                nib_lanes<4>(cell[t][wd], l + n);
+                nib_lanes_g1<4>(cell[t][wd], l + n);
 #pragma unroll
-                for (int q = 0; q < 2; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 2; }
+                for (int q = 0; q < 2; ++q) { cb[n + q] = wd * 8 + q; st[n + q] = 2; sc[n + q] = q ? 16.0f : 1.0f; }
                 n += 2;
             } else {
-                nib_lanes<2>(cell[t][wd], l + n);
+                nib_lanes_g1<2>(cell[t][wd], l + n);
                 cb[n] = wd * 8;
                 st[n] = 1;
+                sc[n] = 1.0f;
                 n += 1;
             }
         }
 #pragma unroll
         for (int i = 0; i < NL; ++i) S[i] = t == 0 ? l[i] * wt[0] : S[i] + l[i] * wt[t];
         if (t == 3) {
+            // value = (S / scale - 256 (N/2 - 1)) / (256 N) with S read as 2^23 + S (exact)
             constexpr float SC = 1.0f / (256.0f * 16.0f);
-            constexpr float BI = -(8388608.0f + 256.0f * 7.0f) / (256.0f * 16.0f);
 #pragma unroll
             for (int i = 0; i < NL; ++i) {
-                v[cb[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7610)), SC, BI);
-                v[cb[i] + st[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7632)), SC, BI);
+                const float sci = SC / sc[i], bi = -(8388608.0f / sc[i] + 256.0f * 7.0f) * SC;
+                v[cb[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7610)), sci, bi);
+                v[cb[i] + st[i]] = fmaf(__uint_as_float(__byte_perm(S[i], 0x4B000000u, 0x7632)), sci, bi);
             }
         }
     }
