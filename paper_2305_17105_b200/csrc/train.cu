@@ -358,7 +358,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     int* s_csh = s_ts + NTC_MAX_CROPS + 1;  // log2 of the crop width when it is a power of 2, else -1
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int slot = warp >> 3, h = (warp >> 2) & 1, q = warp & 3, row = q * 32 + lane;
+    // slot and the TMEM base go through a shuffle: provably warp-uniform, so the MMA-issuing
+    // thread keeps its descriptors in uniform registers (no R2UR waterfall per tcgen05.mma)
+    const int slot = __shfl_sync(0xffffffffu, warp >> 3, 0), h = (warp >> 2) & 1, q = warp & 3, row = q * 32 + lane;
     const int c = CT ? CT : p.c;
 
     // ---- weight images (fp16, SW128 K-major, built once per step by the trailing blocks of
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
 
     // TMEM per slot: depth 1: [0,128) dW-a accumulator, [128,144) dW-b, [192,256) scratch;
     // depth 2: [0,128) dW-a, [128,192) dW-m (the middle layer), [192,208) dW-b, [256,320) scratch
-    const uint32_t tbase = *s_tmem + (uint32_t)slot * (512u / SLOTS);
+    const uint32_t tbase = __shfl_sync(0xffffffffu, *s_tmem, 0) + (uint32_t)slot * (512u / SLOTS);
     const uint32_t t_acc_a = tbase, t_acc_m = tbase + 128, t_acc_b = tbase + (HM == 1 ? 128 : 192);
     const uint32_t t_s = tbase + (SLOTS == 2 ? 192 : 256);  // 64 (two slots) or 128 scratch columns
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
