@@ -13,5 +13,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
 NCU="ncu --set full --clock-control none --import-source on -c 1"
 $NCU -k regex:'decode_kernel' -s 3 -o $O/prof_dec_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras > /dev/null 2>&1
 $NCU -k regex:'train_kernel' -s 3 -o $O/prof_tr_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras > /dev/null 2>&1
-$NCU -k regex:'decode_multi_kernel' -s 1 -o $O/prof_multi_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+# the three full captures together can exceed gpurun's 64 MiB copy-back: MULTI=only / MULTI=skip
+[ "${MULTI:-}" != skip ] && $NCU -k regex:'decode_multi_kernel' -s 1 -o $O/prof_multi_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ls $O | grep $TAG
