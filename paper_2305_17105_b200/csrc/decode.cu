@@ -561,7 +561,10 @@ cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cuda
         using PP = decltype(pr);
         constexpr int HMv = decltype(h)::value;
         using SS = DecodeSmem<PP, HMv>;
-        auto* k = decode_kernel<PP, HMv, decltype(a)::value>;
+        // mip tiles (mode 0) run an instantiation compiled for that mode (no query branches,
+        // uniform-register MMA issue); queries the general one
+        auto* k = p.mode == 0 ? decode_kernel<PP, HMv, decltype(a)::value, 0, true>
+                              : decode_kernel<PP, HMv, decltype(a)::value>;
         // the bench's headline material (NTC 0.2, [57,64,64,9], hardGELU) gets its channel
         // count (and, for mip tiles, the mode) compiled into the kernel
         if constexpr (std::is_same<PP, NTC02>::value && HMv == 1 && decltype(a)::value == 0)
