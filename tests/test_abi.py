@@ -118,3 +118,15 @@ def test_train_footprint_matches_oracle(O, libpath, mip):
                     want.add((ti[0], 0, ti[1 + 2 * t], ti[2 + 2 * t]))
                     want.add((ti[0], 1, ti[9 + 2 * t], ti[10 + 2 * t]))
     assert got == want
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No CPU fallback: with the CUDA library absent every call raises instead of computing."""
+    import paper_2305_17105_b200 as ntc
+
+    monkeypatch.setattr(ntc, "_lib", None)
+    monkeypatch.setattr(ntc, "LIB_PATH", "/nonexistent/libntc.so")
+    with pytest.raises(RuntimeError, match="library missing"):
+        ntc.lib()
+    with pytest.raises(RuntimeError, match="library missing"):
+        ntc.ntc_chain_texels(Profile.named("ntc0.2", 64, 8))
