@@ -618,34 +618,42 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         }
         if (tile + tstride < p.n_tiles) fetch(tile + tstride, F);  // next tile's loads in flight
         wait_mma();
+        // two 16-column tcgen05.ld per half, the second in flight while the first is processed
+        // (the register-dependent wait orders the uses after it)
         auto hidden_epilogue = [&](uint32_t tH, uint32_t tG, const float* bias) {
-            uint32_t r[32];
-            tmem_ld32(t_s + lane_off + 32 * h, r);
-            tmem_wait_ld();
-            uint32_t hv[16], gv[16];
+            uint32_t r[2][16];
+            tmem_ld16(t_s + lane_off + 32 * h, r[0]);
+            tmem_wait_ld_r16(r[0]);
+            tmem_ld16(t_s + lane_off + 32 * h + 16, r[1]);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                float z0 = __uint_as_float(r[2 * i]), z1 = __uint_as_float(r[2 * i + 1]);
-                if (bias) {
-                    const float2 zb = __fadd2_rn(make_float2(z0, z1),
-                                                 *reinterpret_cast<const float2*>(bias + 32 * h + 2 * i));
-                    z0 = zb.x;
-                    z1 = zb.y;
-                }
-                if constexpr (ACT == 0) {
-                    hgelu_and_grad2(z0, z1, hv[i], gv[i]);
-                } else {
-                    float h0, h1, g0, g1;
-                    act_and_grad<ACT>(z0, h0, g0);
-                    act_and_grad<ACT>(z1, h1, g1);
-                    hv[i] = h2u(h0, h1);
-                    gv[i] = h2u(g0, g1);
-                }
-            }
+            for (int part = 0; part < 2; ++part) {
+                if (part == 1) tmem_wait_ld_r16(r[1]);
+                uint32_t hv[8], gv[8];
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                sts_row_chunk(tH, row, 4 * h + cc, hv[4 * cc], hv[4 * cc + 1], hv[4 * cc + 2], hv[4 * cc + 3]);
-                sts_row_chunk(tG, row, 4 * h + cc, gv[4 * cc], gv[4 * cc + 1], gv[4 * cc + 2], gv[4 * cc + 3]);
+                for (int i = 0; i < 8; ++i) {
+                    float z0 = __uint_as_float(r[part][2 * i]), z1 = __uint_as_float(r[part][2 * i + 1]);
+                    if (bias) {
+                        const float2 zb = __fadd2_rn(
+                            make_float2(z0, z1), *reinterpret_cast<const float2*>(bias + 32 * h + 16 * part + 2 * i));
+                        z0 = zb.x;
+                        z1 = zb.y;
+                    }
+                    if constexpr (ACT == 0) {
+                        hgelu_and_grad2(z0, z1, hv[i], gv[i]);
+                    } else {
+                        float h0, h1, g0, g1;
+                        act_and_grad<ACT>(z0, h0, g0);
+                        act_and_grad<ACT>(z1, h1, g1);
+                        hv[i] = h2u(h0, h1);
+                        gv[i] = h2u(g0, g1);
+                    }
+                }
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int ch = 4 * h + 2 * part + cc;
+                    sts_row_chunk(tH, row, ch, hv[4 * cc], hv[4 * cc + 1], hv[4 * cc + 2], hv[4 * cc + 3]);
+                    sts_row_chunk(tG, row, ch, gv[4 * cc], gv[4 * cc + 1], gv[4 * cc + 2], gv[4 * cc + 3]);
+                }
             }
         };
         hidden_epilogue(tH1, tG1, nullptr);
@@ -706,23 +714,29 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         }
         wait_mma();
         auto delta_epilogue = [&](uint32_t tG) {  // delta = fp16(dH) * hardGELU'(Z), in place
-            uint32_t r[32];
-            tmem_ld32(t_s + lane_off + 32 * h, r);
-            tmem_wait_ld();
+            uint32_t r[2][16];
+            tmem_ld16(t_s + lane_off + 32 * h, r[0]);
+            tmem_wait_ld_r16(r[0]);
+            tmem_ld16(t_s + lane_off + 32 * h + 16, r[1]);
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                const uint4 gq = lds_row_chunk(tG, row, 4 * h + cc);
-                const uint32_t gw[4] = {gq.x, gq.y, gq.z, gq.w};
-                uint32_t o[4];
+            for (int part = 0; part < 2; ++part) {
+                if (part == 1) tmem_wait_ld_r16(r[1]);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const __half2 g2 = *reinterpret_cast<const __half2*>(&gw[e]);
-                    const int col = 8 * cc + 2 * e;
-                    const uint32_t aw = h2u(__uint_as_float(r[col]), __uint_as_float(r[col + 1]));
-                    const __half2 dv = __hmul2(*reinterpret_cast<const __half2*>(&aw), g2);
-                    o[e] = *reinterpret_cast<const uint32_t*>(&dv);
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int ch = 4 * h + 2 * part + cc;
+                    const uint4 gq = lds_row_chunk(tG, row, ch);
+                    const uint32_t gw[4] = {gq.x, gq.y, gq.z, gq.w};
+                    uint32_t o[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const __half2 g2 = *reinterpret_cast<const __half2*>(&gw[e]);
+                        const int col = 8 * cc + 2 * e;
+                        const uint32_t aw = h2u(__uint_as_float(r[part][col]), __uint_as_float(r[part][col + 1]));
+                        const __half2 dv = __hmul2(*reinterpret_cast<const __half2*>(&aw), g2);
+                        o[e] = *reinterpret_cast<const uint32_t*>(&dv);
+                    }
+                    sts_row_chunk(tG, row, ch, o[0], o[1], o[2], o[3]);
                 }
-                sts_row_chunk(tG, row, 4 * h + cc, o[0], o[1], o[2], o[3]);
             }
         };
         delta_epilogue(tGL);  // the last G tile now holds its delta
