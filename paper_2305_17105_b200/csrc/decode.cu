@@ -266,7 +266,10 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     // addresses in uniform registers (no R2UR waterfall around each tcgen05.mma).  Measured
     // +2.7% on the headline chain decode; the query/multi instantiations ran slower with it
     // (more spills), so they keep the plain values.
-    const int wg = TILED ? __shfl_sync(0xffffffffu, warp >> 2, 0) : warp >> 2, q = warp & 3, row = q * 32 + lane;
+    // uniform-register MMA issue (shuffled wg / TMEM base) and pipelined TMEM reads: mip
+    // tiles and the compiled multi-material kernel; A/B-measured slower for the query kernel
+    constexpr bool UNI = TILED || (MULTI && CT != 0);
+    const int wg = UNI ? __shfl_sync(0xffffffffu, warp >> 2, 0) : warp >> 2, q = warp & 3, row = q * 32 + lane;
 
     if (!MULTI)
         for (uint32_t i = tid; i < S::WIMG / 16; i += blockDim.x) reinterpret_cast<uint4*>(s_w)[i] = p.wimg[i];
@@ -289,7 +292,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     __syncthreads();
     tc_fence_after();
 
-    const uint32_t tmem = TILED ? __shfl_sync(0xffffffffu, *s_tmem, 0) : *s_tmem;
+    const uint32_t tmem = UNI ? __shfl_sync(0xffffffffu, *s_tmem, 0) : *s_tmem;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;   // this warp's TMEM lane quarter
     const uint32_t w1 = smem_u32(s_w), w2 = w1 + S::W1_BYTES, w3 = w2 + HM * S::W2_BYTES;
     // descriptors advance by (bytes >> 4) in their low 14-bit start-address field
@@ -365,7 +368,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         // pipelined TMEM loads for NTC 0.2 mip tiles (+4.9% on the headline chain); the query
         // and multi-material instantiations measured neutral / -2.4% with them, the two-
         // warpgroup K1 > 64 profiles (255 registers, no spills to remove) about -1.5%
-        epilogue_hidden<ACT, TILED && P::K1_ATOMS == 1>(C.tcol + lane_off, C.abuf, row);
+        epilogue_hidden<ACT, UNI && P::K1_ATOMS == 1>(C.tcol + lane_off, C.abuf, row);
         fence_proxy_async_smem();
         tc_fence_before();
         handoff(C);
