@@ -67,8 +67,8 @@ const char* ntc_last_error(void);
 
 /* ---------------------------------------------------------------- geometry (host, pure)
  * Mip chain down to 1x1 (Table 1).  Feature levels: levels continue while
- * G1 is >= 1x1; mips 0-3 -> level 0, then pairs, the last level takes the tail (PAPER.md:396,
- * R7); r0 = W/ratio/4^j, r1 = r0/2 (Table 1, R8).  Latents/codes of all grids live in one
+ * G1 is >= 1x1, up to ceil((M-3)/2) levels for M mips; mips 0-3 -> level 0, then pairs, the
+ * last level takes the bottom 2-3 mips (R7); r0 = W/ratio/4^j, r1 = r0/2 (Table 1, R8).  Latents/codes of all grids live in one
  * canonical array: grids [F0.G0, F0.G1, F1.G0, ...], each (y, x, ch) row-major.            */
 int32_t ntc_num_mips(const ntc_desc* d);
 int32_t ntc_num_levels(const ntc_desc* d);

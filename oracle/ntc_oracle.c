@@ -25,13 +25,20 @@ static int32_t ilog2(int32_t v) { int32_t l = 0; while ((1 << (l + 1)) <= v) ++l
 /* Mip chain down to 1x1: Table 1 lists mips 0..10 for 1024^2. */
 int32_t ntco_num_mips(int32_t width) { return ilog2(width) + 1; }
 
-/* R7: levels continue while G_1 is at least 1x1, i.e. while floor((W/ratio)/4^j) >= 2
- * ("the last feature level ... cannot be further downsampled").      */
+/* R7: a new level is added while G_1 is still at least 1x1, i.e. while
+ * floor((W/ratio)/4^j) >= 2 ("it cannot be further downsampled"), but not
+ * past the level that holds the bottom mips: "the last feature level represents the bottom
+ * three mip levels", so with M mips (0-3 | pairs | tail of 2-3) there are at
+ * most ceil((M-3)/2) levels.  The cap binds only for the ratio-2 profiles at even log2 sizes
+ * (e.g. 4096^2 NTC 1.0: 5 levels, mips 10-12 on the last).                 */
 int32_t ntco_num_levels(const ntco_desc* d) {
     int32_t L = 0;
     int64_t r0 = d->width / d->g0_ratio;
     while (r0 >= 2) { ++L; r0 /= 4; }
-    return L;
+    int32_t M = ntco_num_mips(d->width);
+    int32_t Lm = (M - 3 + 1) / 2;
+    if (Lm < 1) Lm = 1;
+    return L < Lm ? L : Lm;
 }
 
 /* R7: "the first feature level must represent all higher resolution mips (levels 0 to 3),

@@ -106,16 +106,23 @@ class Compressor:
         crops = np.stack([x0, y0, np.full(cfg.crops, cs), np.full(cfg.crops, cs)], 1).astype(np.int32)
         return make_batch(m, crops, self.ref[m], wm * d.channels)
 
-    def step(self, frozen: bool, record: bool = False):
+    def plan(self, frozen: bool):
+        """The next step's batch and hyper-parameters: LOD + crops, cosine
+        learning rates; noise on and latents trained in the noisy phase, noise
+        off and latents frozen after the explicit quantisation (R25)."""
         cfg = self.cfg
         self.step_no += 1
         t = self.step_no
         hp = Hparams(lr_at(t - 1, self.total, cfg.lr_latent), lr_at(t - 1, self.total, cfg.lr_weight), 0.9, 0.999,
                      1e-8, t, cfg.seed, 0 if frozen else 1, 0, 1 if frozen else 0)
-        ntc_train_step(self.trainer, self.buf, self._batch(), hp, self.loss, self.status,
+        return self._batch(), hp
+
+    def step(self, frozen: bool, record: bool = False):
+        batch, hp = self.plan(frozen)
+        ntc_train_step(self.trainer, self.buf, batch, hp, self.loss, self.status,
                        flags=NTC_STEP_GRADS | NTC_STEP_APPLY)
         if record:
-            self.losses.append((t, float(self.loss.item())))
+            self.losses.append((self.step_no, float(self.loss.item())))
 
     def freeze(self):
         """Explicit quantisation; latents become their bin centres."""

@@ -52,7 +52,8 @@ static int ilog2i(int64_t v) {
     return l;
 }
 
-static ntc_status check_desc(const ntc_desc* d) {
+namespace ntc {
+ntc_status check_desc(const ntc_desc* d) {
     if (!d) return fail(NTC_ERR_INVALID_ARGUMENT, "desc is NULL");
     if (d->width < 4 || d->width > (1 << 15) || (d->width & (d->width - 1)))
         return fail(NTC_ERR_INVALID_ARGUMENT, "width %d must be a power of two in [4, 32768]", d->width);
@@ -67,13 +68,16 @@ static ntc_status check_desc(const ntc_desc* d) {
     if (profile_id(d) < 0) return fail(NTC_ERR_UNSUPPORTED, "profile (C0=%d,B0=%d,C1=%d,B1=%d) not compiled", d->c0, d->b0, d->c1, d->b1);
     return NTC_OK;
 }
+}  // namespace ntc
 
 extern "C" int32_t ntc_num_mips(const ntc_desc* d) { return ilog2i(d->width) + 1; }
 
 extern "C" int32_t ntc_num_levels(const ntc_desc* d) {
     int32_t L = 0;
     for (int64_t r = d->width / d->g0_ratio; r >= 2; r /= 4) ++L;  // G1 = r/2 >= 1 (R7)
-    return L;
+    // ... and no level past the one holding the bottom 2-3 mips (R7)
+    const int32_t Lm = (ilog2i(d->width) - 1) / 2 > 1 ? (ilog2i(d->width) - 1) / 2 : 1;  // ceil((M-3)/2)
+    return L < Lm ? L : Lm;
 }
 
 extern "C" int32_t ntc_level_of_mip(const ntc_desc* d, int32_t mip) {

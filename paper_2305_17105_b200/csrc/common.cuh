@@ -1,6 +1,11 @@
 // common.cuh -- shared host/device definitions of the NTC CUDA path (product code).
 #pragma once
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
+
+#include <cuda_runtime.h>
 
 #include "../../include/ntc.h"
 
@@ -87,5 +92,20 @@ struct MultiTable {
     const int32_t* perm;    // query indices grouped by material
     MatRec rec[NTC_MAX_MATERIALS];
 };
+
+// Raise a kernel's dynamic-SMEM limit once per (device, kernel, size) instead of on every
+// launch (cudaFuncSetAttribute is a driver call; the hot-path entry points are called per step).
+inline cudaError_t ensure_smem(const void* kernel, uint32_t bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<std::pair<int, const void*>, uint32_t>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(std::make_pair(dev, kernel), bytes);
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(key)) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
+}
 
 }  // namespace ntc

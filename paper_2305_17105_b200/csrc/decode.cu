@@ -600,7 +600,7 @@ cudaError_t launch_decode(int pid, int hm, const DecodeParams& p, int grid, cuda
         // and the 16-channel material of the random-access line (configs[2])
         if constexpr (std::is_same<PP, NTC02>::value && HMv == 1 && decltype(a)::value == 0)
             if (p.c == 16) k = p.mode == 0 ? decode_kernel<PP, HMv, 0, 16, true> : decode_kernel<PP, HMv, 0, 16>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
+        cudaError_t e = ensure_smem((const void*)k, SS::BYTES);
         if (e != cudaSuccess) return e;
         k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p);
         return cudaGetLastError();
@@ -617,7 +617,7 @@ cudaError_t launch_decode_multi(int pid, int hm, const DecodeParams& p, const Mu
         // the 8-channel materials of the multi-material line (Table 4 analog)
         if constexpr (std::is_same<PP, NTC02>::value && HMv == 1 && decltype(a)::value == 0)
             if (p.c == 8) k = decode_multi_kernel<PP, HMv, 0, 8>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::BYTES);
+        cudaError_t e = ensure_smem((const void*)k, SS::BYTES);
         if (e != cudaSuccess) return e;
         k<<<grid, SS::NWG * 128, SS::BYTES, s>>>(p, mt);
         return cudaGetLastError();

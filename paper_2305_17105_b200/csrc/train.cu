@@ -57,7 +57,6 @@ struct TrainParams {
     float* partial;     // [grid][P]
     float* loss_partial;  // [grid * slots]
     int32_t P;
-    int32_t debug_flags;  // profiling only (NTC_DEBUG_TRAIN env): 1 = skip the latent scatter
     int32_t freeze;       // frozen phase: no latent gradients
 };
 
@@ -805,7 +804,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // vector reductions -- no global contention storm.
         {
             const float s = p.inv_bc;
-            const bool on = valid && !(p.debug_flags & 1) && !p.freeze;
+            const bool on = valid && !p.freeze;
             if (h == 0) {
                 uint32_t r[4 * C0];
 #pragma unroll
@@ -1226,6 +1225,7 @@ extern "C" ntc_status ntc_grid_layout(const ntc_desc* d, int32_t level, int32_t*
                                       int64_t* off1);
 namespace ntc {
 ntc_status api_fail(ntc_status s, const char* msg);
+ntc_status check_desc(const ntc_desc* d);
 uint16_t host_f16(double v);
 double host_tri(double t);
 }  // namespace ntc
@@ -1274,6 +1274,7 @@ static void train_dispatch(const ntc_desc* d, F&& f) {
 
 extern "C" ntc_status ntc_trainer_create(const ntc_desc* d, ntc_trainer** out) {
     if (!d || !out) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (ntc_status s = check_desc(d)) return s;  // same validation as every decode entry point
     if (train_profile(d) < 0 || (d->hidden_mats != 1 && d->hidden_mats != 2) ||
         (d->activation != 0 && d->activation != 1))
         return api_fail(NTC_ERR_UNSUPPORTED, "training kernel compiled for the Table 2 profiles, depth 1 or 2, hardGELU or GELU");
@@ -1414,16 +1415,21 @@ extern "C" int32_t ntc_train_footprint(const ntc_desc* d, const ntc_batch* batch
     return (int32_t)boxes.size();
 }
 
+// prefix sums of the boxes' latent counts; the kernels index footprints with int32, so a
+// footprint past INT32_MAX latents (e.g. one full-mip crop of a 32768^2 NTC 2.25 texture)
+// is refused (-1) instead of wrapping
 static int32_t box_prefix(const std::vector<Box>& boxes, Box* dst, int32_t* start) {
     int64_t acc = 0;
     for (size_t i = 0; i < boxes.size(); ++i) {
         dst[i] = boxes[i];
         start[i] = (int32_t)acc;
         acc += (int64_t)(boxes[i].x1 - boxes[i].x0 + 1) * (boxes[i].y1 - boxes[i].y0 + 1) * boxes[i].C;
+        if (acc > INT32_MAX) return -1;
     }
     start[boxes.size()] = (int32_t)acc;
     return (int32_t)acc;
 }
+#define FOOTPRINT_TOO_BIG() api_fail(NTC_ERR_UNSUPPORTED, "batch footprint exceeds 2^31-1 latents")
 
 // packed <-> dense copy over footprint boxes (data-parallel latent exchanges):
 // mode 0 pack, 1 unpack (src NULL: zero), 2 unpack-add
@@ -1436,8 +1442,8 @@ __global__ void footprint_copy_kernel(const __grid_constant__ PrepParams p, cons
     box_locate(p.box, p.box_start, p.nbox, i, b, li);
     if (mode == 1)
         dst[li] = src ? src[i] : 0.0f;
-    else if (mode == 2)
-        dst[li] += src[i];
+    else if (mode == 2)  // boxes of different senders may overlap: the adds must not race
+        atomicAdd(dst + li, src[i]);
     else
         dst[i] = src[li];
 }
@@ -1459,6 +1465,7 @@ static ntc_status footprint_copy(const ntc_desc* d, const ntc_batch* batch, cons
     const std::vector<Box> boxes = footprint(d, batch);
     pp.nbox = (int32_t)boxes.size();
     const int32_t n = box_prefix(boxes, pp.box, pp.box_start);
+    if (n < 0) return FOOTPRINT_TOO_BIG();
     if (n == 0) return NTC_OK;
     footprint_copy_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(pp, src, dst, unpack);
     cudaError_t e = cudaGetLastError();
@@ -1514,6 +1521,7 @@ extern "C" ntc_status ntc_boxes_copy(const ntc_desc* d, const int32_t* boxes, in
     memset(&pp, 0, sizeof pp);
     pp.nbox = (int32_t)bx.size();
     const int32_t cnt = box_prefix(bx, pp.box, pp.box_start);
+    if (cnt < 0) return FOOTPRINT_TOO_BIG();
     if (cnt == 0) return NTC_OK;
     const int km = mode == NTC_BOX_PACK ? 0 : mode == NTC_BOX_ADD ? 2 : 1;
     footprint_copy_kernel<<<(cnt + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
@@ -1558,6 +1566,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         memset(&pp, 0, sizeof pp);
         pp.nbox = (int32_t)boxes.size();
         const int32_t n = box_prefix(boxes, pp.box, pp.box_start);
+        if (n < 0) return FOOTPRINT_TOO_BIG();
         pp.latents = buf->latents;
         pp.noisy = reinterpret_cast<__half*>(buf->noisy);
         pp.grad_lat = buf->grad_lat;
@@ -1624,7 +1633,6 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.partial = t->partial;
         tp.loss_partial = t->loss_partial;
         tp.P = (int32_t)P;
-        if (const char* dbg = getenv("NTC_DEBUG_TRAIN")) tp.debug_flags = atoi(dbg);
         tp.freeze = hp->freeze_latents;
         int slots = 1;
         uint32_t smem_bytes = 0;
@@ -1643,7 +1651,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         });
         const int grid = (int)std::min<int64_t>(std::min<int64_t>(t->num_sms, 8 * RED_MAXK),
                                                 (tiles + slots - 1) / slots);
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+        e = ensure_smem((const void*)k, smem_bytes);
         if (e == cudaSuccess) {
             k<<<grid, slots * 256, smem_bytes, st>>>(tp);
             // t6: deterministic cross-CTA reduction, scaled by 1/(B c); with APPLY in the same
@@ -1654,6 +1662,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
             if ((flags & NTC_STEP_APPLY) && apply_buffers_ok(buf)) {
                 AdamParams a;
                 const int64_t nlat = build_adam(d, buf, boxes, hp, a);
+                if (nlat < 0) return FOOTPRINT_TOO_BIG();
                 reduce_adam_kernel<<<rblocks + (int)((nlat + 256 * LPT - 1) / (256 * LPT)), 256, 0, st>>>(ra, a,
                                                                                                     rblocks);
                 e = cudaGetLastError();
@@ -1677,6 +1686,7 @@ static int64_t build_adam(const ntc_desc* d, const ntc_train_buffers* buf, const
     memset(&a, 0, sizeof a);
     a.nbox = (int32_t)boxes.size();
     const int32_t n = box_prefix(boxes, a.box, a.box_start);
+    if (n < 0) return -1;
     a.dense_latents = hp->dense_latent_adam;
     a.n_latents = NL;
     a.P = (int32_t)P;
@@ -1722,7 +1732,9 @@ static ntc_status apply_step(const ntc_desc* d, const ntc_train_buffers* buf, co
                              const ntc_train_hparams* hp, cudaStream_t st) {
     if (!apply_buffers_ok(buf)) return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
     AdamParams a;
-    const int64_t total = ntc_num_params(d) + (build_adam(d, buf, boxes, hp, a) + LPT - 1) / LPT;
+    const int64_t nlat = build_adam(d, buf, boxes, hp, a);
+    if (nlat < 0) return FOOTPRINT_TOO_BIG();
+    const int64_t total = ntc_num_params(d) + (nlat + LPT - 1) / LPT;
     adam_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? NTC_OK : api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));

@@ -69,10 +69,17 @@ def test_host_validation_without_gpu(libpath):
     L = ntc.lib()
     bad_profile = ntc.make_desc(Profile(64, 8, 4, 6, 3, 12, 4))
     assert L.ntc_quantize_latents(ctypes.byref(bad_profile), None, None, None) == ntc.NTC_ERR_UNSUPPORTED
-    for bad in (Profile(63, 8), Profile(64, 0), Profile(64, 17), Profile(64, 8, 3), Profile(64, 8, hidden_mats=3)):
+    for bad, msg in ((Profile(63, 8), b"width"), (Profile(64, 0), b"channels"), (Profile(64, 17), b"channels"),
+                     (Profile(64, 8, 3), b"g0_ratio"), (Profile(64, 8, 0), b"g0_ratio"),
+                     (Profile(64, 8, hidden_mats=3), b"hidden_mats")):
         assert L.ntc_quantize_latents(ctypes.byref(ntc.make_desc(bad)), None, None, None) == \
             ntc.NTC_ERR_INVALID_ARGUMENT
-    assert b"width" in L.ntc_last_error() or True
+        assert msg in L.ntc_last_error(), (bad, L.ntc_last_error())
+        # the trainer validates the same descriptor before touching the device
+        out = ctypes.c_void_p()
+        assert L.ntc_trainer_create(ctypes.byref(ntc.make_desc(bad)), ctypes.byref(out)) == \
+            ntc.NTC_ERR_INVALID_ARGUMENT
+        assert msg in L.ntc_last_error(), (bad, L.ntc_last_error())
     ok = ntc.make_desc(Profile.named("ntc0.2", 64, 8))
     assert L.ntc_quantize_latents(ctypes.byref(ok), None, None, None) == ntc.NTC_ERR_INVALID_ARGUMENT
     assert L.ntc_decode_chain(None, None, None) == ntc.NTC_ERR_INVALID_ARGUMENT

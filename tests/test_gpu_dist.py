@@ -56,6 +56,14 @@ def _setup():
     return d, lat, par, ref, gcrops
 
 
+def _setup_chain():
+    """_setup's material with the whole reference mip chain (fp16 bits per mip)."""
+    from paper_2305_17105_b200.synth import box_mip_chain_u8, gen_reference_u8, u8_to_f16_bits
+
+    d, lat, par, _, _ = _setup()
+    return d, lat, par, [u8_to_f16_bits(m) for m in box_mip_chain_u8(gen_reference_u8(3, 128, 8))]
+
+
 def _worker(rank, world, port, q):
     import sys
 
@@ -113,7 +121,7 @@ def test_dp_step_two_ranks_matches_single_batch():
     assert np.array_equal(res[0][4], res[1][4]) and np.array_equal(res[0][5], res[1][5])
 
 
-def _shard_worker(rank, world, port, q, steps):
+def _shard_worker(rank, world, port, q, steps, mip=0, crop=32):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -125,13 +133,14 @@ def _shard_worker(rank, world, port, q, steps):
         from paper_2305_17105_b200.dist import ShardedDataParallelTrainer
         from paper_2305_17105_b200.synth import gen_crops
 
-        d, lat, par, ref, _ = _setup()
+        d, lat, par, ref = _setup_chain()
         tr = ShardedDataParallelTrainer(d, torch.from_numpy(lat).to(DEV), torch.from_numpy(par).to(DEV))
-        refd = torch.from_numpy(ref.view(np.int16)).to(DEV)
+        refd = [torch.from_numpy(r.view(np.int16)).to(DEV) for r in ref]
         losses = []
         for s in range(steps):
             hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, s + 1, 7, 1, 0)
-            losses.append(float(tr.step(0, gen_crops(40 + s, 128, 0, 6, 32), refd, 128 * 8, hp).item()))
+            crops = gen_crops(40 + s, 128, mip, 6, crop)
+            losses.append(float(tr.step(mip, crops, refd[mip], (128 >> mip) * 8, hp).item()))
         full = tr.gather_latents()
         torch.cuda.synchronize()
         q.put((rank, losses, tr.t["params"].cpu().numpy().copy(), full.cpu().numpy().copy()))
@@ -139,35 +148,39 @@ def _shard_worker(rank, world, port, q, steps):
         dist.destroy_process_group()
 
 
-def test_sharded_dp_matches_single_process():
-    """Latent grids sharded by row bands (2 ranks): after 3 GRADS+APPLY steps the gathered
+@pytest.mark.parametrize("world,mip,crop", [(2, 0, 32), (3, 3, 12), (3, 4, 6)])
+def test_sharded_dp_matches_single_process(world, mip, crop):
+    """Latent grids sharded by row bands (2-3 ranks): after 3 GRADS+APPLY steps the gathered
     latents and the weights equal single-process training on the same global batches (fp32
-    summation order only), and the two ranks agree."""
+    summation order only), and the ranks agree.  At mips 3-4 every crop spans several bands,
+    so boxes that different readers send back to one owner overlap (their halo-gradient adds
+    must not race: ADVICE r1)."""
     from paper_2305_17105_b200.synth import gen_crops
 
     steps = 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q, steps)) for r in range(2)]
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q, steps, mip, crop)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda r: r[0])
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    d, lat, par, ref, _ = _setup()
+    d, lat, par, ref = _setup_chain()
     NL, P = lat.size, par.size
     t = {k: torch.zeros(NL, device=DEV) for k in ("m_lat", "v_lat", "grad_lat", "noisy")}
     t.update({k: torch.zeros(P, device=DEV) for k in ("m_par", "v_par", "grad_par")})
     t["latents"] = torch.from_numpy(lat.copy()).to(DEV)
     t["params"] = torch.from_numpy(par.copy()).to(DEV)
-    refd = torch.from_numpy(ref.view(np.int16)).to(DEV)
+    refd = [torch.from_numpy(r.view(np.int16)).to(DEV) for r in ref]
     tr, bufs, loss = ntc.Trainer(d), ntc.make_buffers(t), torch.zeros(1, device=DEV)
     losses = []
     for s in range(steps):
         hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, s + 1, 7, 1, 0)
-        ntc.ntc_train_step(tr, bufs, ntc.make_batch(0, gen_crops(40 + s, 128, 0, 6, 32), refd, 128 * 8), hp, loss)
+        crops = gen_crops(40 + s, 128, mip, 6, crop)
+        ntc.ntc_train_step(tr, bufs, ntc.make_batch(mip, crops, refd[mip], (128 >> mip) * 8), hp, loss)
         losses.append(float(loss.item()))
     torch.cuda.synchronize()
     ref_lat, ref_par = t["latents"].cpu().numpy(), t["params"].cpu().numpy()
@@ -175,7 +188,8 @@ def test_sharded_dp_matches_single_process():
         assert np.allclose(l, losses, rtol=1e-5)
         assert np.allclose(p, ref_par, rtol=1e-4, atol=1e-6)
         assert np.allclose(full, ref_lat, rtol=1e-4, atol=1e-6)
-    assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
+    for r in res[1:]:
+        assert np.array_equal(res[0][2], r[2]) and np.array_equal(res[0][3], r[3])
 
 
 def test_bench_two_ranks_json_line():

@@ -44,15 +44,30 @@ def test_spec_level_examples(O):
     L = O.num_levels(d13)
     assert [m for m in range(13) if O.level_of_mip(d13, m) == L - 1] == [10, 11, 12]
     assert O.level_of_mip(d13, 12) == 4
-    # every level but the first and the last serves exactly two mips
-    for W in (256, 1024, 4096, 8192):
-        d = Profile.named("ntc0.2", W, 8)
-        L = O.num_levels(d)
-        groups = [[m for m in range(O.num_mips(W)) if O.level_of_mip(d, m) == j] for j in range(L)]
-        assert groups[0] == [0, 1, 2, 3]
-        for g in groups[1:-1]:
-            assert len(g) == 2
-        assert sorted(sum(groups, [])) == list(range(O.num_mips(W)))
+    # SPEC.md:118 "(mip 12, 13 mips) -> level 4" holds for every profile, the ratio-2 ones
+    # (NTC 1.0 / 2.25, G^0_0 = W/2) included: their G1 could shrink once more, but "the last
+    # feature level represents the bottom three mip levels"
+    for name in PROFILES:
+        d = Profile.named(name, 4096, 9)
+        assert O.num_levels(d) == 5
+        assert [O.level_of_mip(d, m) for m in range(13)] == [0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 4]
+        # ... and the Table 1 grouping at 1024^2
+        d = Profile.named(name, 1024, 9)
+        assert [O.level_of_mip(d, m) for m in range(11)] == [0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 3]
+    # every level but the first and the last serves exactly two mips, the last two or three
+    # (PAPER.md:396), for every profile and size
+    for name in PROFILES:
+        for W in (16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192):
+            d = Profile.named(name, W, 8)
+            L = O.num_levels(d)
+            groups = [[m for m in range(O.num_mips(W)) if O.level_of_mip(d, m) == j] for j in range(L)]
+            if L > 1:
+                assert groups[0] == [0, 1, 2, 3]
+                assert all(len(g) == 2 for g in groups[1:-1])
+                assert len(groups[-1]) in (2, 3)
+            assert sorted(sum(groups, [])) == list(range(O.num_mips(W)))
+            # G1 of the last level is at least 1x1 ("cannot be further downsampled")
+            assert O.grid_res(d, L - 1)[1] >= 1 and O.grid_res(d, L - 1)[0] >= 2
 
 
 def test_spec_geometry_examples(O):

@@ -111,29 +111,66 @@ def test_channel_permutation_symmetry(O):
     assert np.allclose(dl1, dl2, rtol=1e-12, atol=1e-18)
 
 
-def test_noise_off_equals_quantised_path_on_centres(O):
-    """With latents at bin centres and noise off, the training forward reads exactly the
-    decode's dequantised values: the train loss equals the loss of the oracle decode
-    (unclamped outputs in range) on the same texels."""
-    d = Profile.named("ntc0.2", 32, 3)
-    lat, par, chain = _material(O, d, 21)
-    codes = O.quantize_latents(d, lat)
-    cent = np.zeros_like(lat)
+def _centres(O, d, codes):
+    """Bin centres of quantised codes, grid by grid: (code - (N/2 - 1)) Q."""
+    cent = np.zeros(codes.shape, np.float32)
     for j in range(O.num_levels(d)):
         for k, B in ((0, d.b0), (1, d.b1)):
             a = O.grid_offset(d, j, k)
             b = O.grid_offset(d, j, 1) if k == 0 else O.grid_offset(d, j + 1, 0)
             cent[a:b] = (codes[a:b].astype(np.float64) - (2**B // 2 - 1)) / 2**B
+    return cent
+
+
+@pytest.mark.parametrize("mip", [0, 2, 4])
+def test_noise_off_equals_quantised_path_on_centres(O, mip):
+    """Pins train_grads' fp16-rounded forward (round_f16 = 1, the R14 path the GPU parity runs
+    against) to the decode oracle: with latents at bin centres and noise off, the training
+    forward reads exactly the decode's dequantised values (R25), so with the gain-0.3 weight
+    recipe (no output clamps -- asserted) the loss equals mean((y - R)^2) of the decoded
+    texels, and db3 equals its per-channel form 2/(B c) sum (y_k - R_k) (R17)."""
+    d = Profile.named("ntc0.2", 32, 3)
+    lat = gen_latents(21, O.num_latents(d))
+    par = gen_weights_f32(22, d.input_dim, d.channels, 1, out_gain=0.3)
+    chain = box_mip_chain_u8(gen_reference_u8(23, 32, 3))
+    cent = _centres(O, d, O.quantize_latents(d, lat))
+    codes = O.quantize_latents(d, cent)
+    assert np.array_equal(_centres(O, d, codes), cent)   # centres are fixed points
     par16 = par.astype(np.float16)
-    ref = u8_to_f16_bits(chain[0])
-    crops = np.array([[0, 0, 32, 32]], np.int32)
-    loss, _, _ = O.train_grads(d, cent, par16.astype(np.float32), 0, crops, ref, 0, 0, noise_on=False)
-    q = np.stack(np.meshgrid(np.arange(32), np.arange(32), indexing="xy"), -1).reshape(-1, 2)
-    q = np.concatenate([q, np.zeros((q.shape[0], 1), np.int64)], 1).astype(np.int32)
+    wm = 32 >> mip
+    ref = u8_to_f16_bits(chain[mip])
+    crops = np.array([[0, 0, wm, wm]], np.int32)
+    loss, dp, dl = O.train_grads(d, cent, par16.astype(np.float32), mip, crops, ref, 0, 0, noise_on=False)
+    q = np.stack(np.meshgrid(np.arange(wm), np.arange(wm), indexing="xy"), -1).reshape(-1, 2)
+    q = np.concatenate([q, np.full((q.shape[0], 1), mip, np.int64)], 1).astype(np.int32)
     y = O.decode_texels(d, codes, par16.view(np.uint16), q)
     R = ref.view(np.float16).astype(np.float64).reshape(-1, 3)
-    if np.all((y > 0) & (y < 1)):
-        assert abs(loss - np.mean((y - R) ** 2)) < 1e-14
+    assert np.all((y > 0) & (y < 1))     # no clamp: decode == unclamped forward
+    assert abs(loss - np.mean((y - R) ** 2)) < 1e-14
+    assert np.allclose(dp[-3:], 2.0 / y.size * np.sum(y - R, 0), rtol=1e-10, atol=1e-15)
+
+
+def test_quantize_latents_per_grid_bits(O):
+    """ntco_quantize_latents assigns each grid its own B (G0: B0, G1: B1; Table 2): compared
+    with the closed-form rule idx = clamp(floor(v 2^B + 1/2), -(N/2 - 1), N/2), code = idx +
+    N/2 - 1 (R9/R10), evaluated in numpy on grid spans computed here from
+    the grid resolutions (Table 1 geometry), for profiles whose B0 and B1 differ."""
+    for name in ("ntc0.2", "ntc0.5", "ntc1.0", "ntc2.25"):
+        d = Profile.named(name, 64, 4)
+        lat = gen_latents(31, O.num_latents(d), scale=0.6)   # spans both clamp ends
+        got = O.quantize_latents(d, lat)
+        want = np.zeros_like(got)
+        off = 0
+        for j in range(O.num_levels(d)):
+            r0, r1 = O.grid_res(d, j)
+            for n, B in ((r0 * r0 * d.c0, d.b0), (r1 * r1 * d.c1, d.b1)):
+                N = 2**B
+                v = lat[off:off + n].astype(np.float64)
+                idx = np.clip(np.floor(v * N + 0.5), -(N // 2 - 1), N // 2)
+                want[off:off + n] = (idx + N // 2 - 1).astype(np.uint8)
+                off += n
+        assert off == lat.size
+        assert np.array_equal(got, want), name
 
 
 def test_adam_matches_torch(O):

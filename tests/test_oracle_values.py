@@ -99,6 +99,21 @@ def test_triangle_wave_fourier(O):
         assert abs(O.tri(t) - series) < 1e-4
 
 
+def test_pe_table_golden(O):
+    """The 8 x 6 per-axis PE table (tests/golden/pe_table.txt): it fixes
+    the phase sign (+1/4 instead of -1/4 moves entries 2/4/6), the octave order and the
+    integer (not texel-centre) position; the last column is the constant the Fig. 5 caption
+    states.  Every (x, y) of a 16 x 16 patch: [PE_x(x mod 8) | PE_y(y mod 8)]."""
+    from conftest import golden
+
+    tab = {int(r[0]): np.array([float(v) for v in r[1:]]) for r in golden("pe_table.txt")}
+    assert sorted(tab) == list(range(8))
+    assert all(t[5] == 0.0 for t in tab.values())  # "the last value is constant"
+    for y in range(16):
+        for x in range(16):
+            assert np.array_equal(O.pe(x, y), np.concatenate([tab[x % 8], tab[y % 8]])), (x, y)
+
+
 def test_pe_properties(O):
     """PAPER.md:464 (tile repeats every 8x8), PAPER.md:468 ('6+6 scalars', 'the last value
     is constant in both the horizontal and vertical encoding')."""
