@@ -284,6 +284,7 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_extras:
         res["random"] = bench_random(args, ntc, torch, dev, flush)
         res["multi"] = bench_multi(args, ntc, torch, dev, flush)
+        res["configs"] = bench_configs(args, ntc, torch, dev, flush)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(d, codes, wts, budget_s=args.cpu_budget)
     return res
@@ -323,6 +324,114 @@ def bench_random(args, ntc, torch, dev, flush):
             "ms_per_step": t * 1e3, "roofline": {"bound": "tensor", "achieved": round(tf, 2),
                                                  "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                                                  "frac": round(tf / pk["bf16_tflops"], 4)}}
+
+
+def _material(ntc, torch, d, seed, dev, out_gain=0.3):
+    return ntc.Material(d, torch.from_numpy(gen_codes(seed, ntc.grid_list(d))).to(dev),
+                        torch.from_numpy(gen_weights_f16(seed + 1, d.input_dim, d.channels, d.hidden_mats,
+                                                         out_gain=out_gain).view(np.int16)).to(dev))
+
+
+def _row(d, texels, t, flops_per_texel, peak, **kw):
+    tf = flops_per_texel * texels / t / 1e12
+    r = {"texels": int(texels), "ms": round(t * 1e3, 4), "Gtexel_s": round(texels / t / 1e9, 3),
+         "tflops": round(tf, 1), "frac": round(tf / peak, 4)}
+    r.update(kw)
+    return r
+
+
+VARIANTS = [("ntc0.5", 1, 0), ("ntc1.0", 1, 0), ("ntc2.25", 1, 0), ("ntc0.2", 2, 0), ("ntc0.2", 1, 1)]
+
+
+def bench_configs(args, ntc, torch, dev, flush):
+    """The other SURVEY.md 8(d) rows, each timed like the headline (L2 flushed before every
+    run, CUDA events on the launching stream, mean of `reps`), with its tensor-roofline
+    fraction (unpadded algorithmic FLOPs / measured burst peak):
+      C1  configs[0]: 256^2 x 8ch, mip 0 only (65,536 texels, one ntc_decode_mip)
+      C2  configs[1]: 2048^2 x 9ch full chain (5,592,405 texels)
+      C3a configs[2]: 4096^2 x 16ch full chain (22,369,621 texels)
+      stress: the headline material with output-layer gain 1.0 (many clamped outputs)
+      C4_lod_mix configs[3]: training steps whose LOD follows the paper's law
+      variants: the other Table 2 profiles, depth reading B and exact GELU, decode and train."""
+    pk, _ = _peaks()
+    peak = pk["bf16_tflops"]
+    reps = max(3, min(args.steps, 10))
+    res = {}
+
+    def chain(name, d, seed, gain=0.3, **kw):
+        mat = _material(ntc, torch, d, seed, dev, gain)
+        T = ntc.ntc_chain_texels(d)
+        out = torch.empty((T * d.channels,), dtype=torch.float16, device=dev)
+        t = _device_time(torch, lambda: ntc.ntc_decode_chain(mat, out), flush, reps)
+        return _row(d, T, t, decode_flops_per_texel(d), peak, **kw)
+
+    d1 = Profile.named("ntc0.2", 256, 8)
+    m1 = _material(ntc, torch, d1, SEED_BASE + 0, dev)
+    o1 = torch.empty((256 * 256 * 8,), dtype=torch.float16, device=dev)
+    t1 = _device_time(torch, lambda: ntc.ntc_decode_mip(m1, 0, o1), flush, reps)
+    res["C1"] = _row(d1, 256 * 256, t1, decode_flops_per_texel(d1), peak,
+                     workload="256^2 x 8ch NTC0.2, mip 0 (configs[0]); one launch, launch-latency bound",
+                     launches=1)
+    res["C2"] = chain("C2", Profile.named("ntc0.2", 2048, 9), SEED_BASE + 1,
+                      workload="2048^2 x 9ch NTC0.2 full chain (configs[1])")
+    res["C3a"] = chain("C3a", Profile.named("ntc0.2", W, 16), SEED_BASE + 2,
+                       workload="4096^2 x 16ch NTC0.2 full chain (configs[2])")
+    res["stress"] = chain("stress", Profile.named("ntc0.2", W, C), SEED_BASE + 4, gain=1.0,
+                          workload="4096^2 x 9ch NTC0.2 full chain, stress weights (output gain 1.0)")
+    res["variants_decode"] = [
+        chain(name, Profile.named(name, W, C, hm, act), SEED_BASE + 4, profile=name, hidden_mats=hm,
+              activation=["hardGELU", "GELU"][act])
+        for name, hm, act in VARIANTS]
+
+    # training: LOD mix (configs[3]) and the variants at LOD 0
+    ref_chain = [torch.from_numpy(u8_to_f16_bits(m).view(np.int16)).to(dev)
+                 for m in box_mip_chain_u8(gen_reference_u8(SEED_BASE + 8, W, C))]
+
+    def trainer(d, seed):
+        NL, P = ntc.ntc_num_latents(d), ntc.ntc_num_params(d)
+        t = {k: torch.zeros(NL, device=dev) for k in ("m_lat", "v_lat", "grad_lat", "noisy")}
+        t.update({k: torch.zeros(P, device=dev) for k in ("m_par", "v_par", "grad_par")})
+        t["latents"] = torch.from_numpy(gen_latents(seed, NL)).to(dev)
+        t["params"] = torch.from_numpy(gen_weights_f32(seed + 1, d.input_dim, d.channels, d.hidden_mats)).to(dev)
+        return ntc.Trainer(d), t, ntc.make_buffers(t), torch.zeros(1, device=dev)
+
+    def train_time(d, batches, seed):
+        tr, t, bufs, loss = trainer(d, seed)
+        step = [0]
+
+        def run_all():
+            for b in batches:
+                step[0] += 1
+                ntc.ntc_train_step(tr, bufs, b, ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, step[0], 7, 1, 0), loss)
+
+        return _device_time(torch, run_all, flush, reps)
+
+    from paper_2305_17105_b200.compress import sample_lod
+
+    d = Profile.named("ntc0.2", W, C)
+    M = ntc.ntc_num_mips(d)
+    rng = np.random.default_rng(SEED_BASE + 9)
+    batches, texels, lods = [], 0, []
+    for _ in range(32):
+        m = sample_lod(rng, M)
+        crops = gen_crops(int(rng.integers(1 << 30)), W, m, 4, 256)
+        texels += int((crops[:, 2] * crops[:, 3]).sum())
+        lods.append(m)
+        batches.append(ntc.make_batch(m, crops, ref_chain[m], (W >> m) * C))
+    tt = train_time(d, batches, SEED_BASE + 10)
+    res["C4_lod_mix"] = _row(d, texels, tt, train_flops_per_texel(d), peak,
+                             workload="4096^2 x 9ch NTC0.2 train steps (GRADS|APPLY), 32 steps of 4 x 256^2 crops "
+                                      "(capped at the mip size) at LODs from the paper's law (PAPER.md:572-574)",
+                             steps=32, lods=lods, unit_note="Gtexel_s = G texels/s over the 32 steps")
+    crops0 = gen_crops(SEED_BASE + 3, W, 0, 4, 256)
+    rows = []
+    for name, hm, act in [("ntc0.2", 1, 0)] + VARIANTS:
+        dv = Profile.named(name, W, C, hm, act)
+        b = [ntc.make_batch(0, crops0, ref_chain[0], W * C)]
+        rows.append(_row(dv, 4 * 256 * 256, train_time(dv, b, SEED_BASE + 11), train_flops_per_texel(dv), peak,
+                         profile=name, hidden_mats=hm, activation=["hardGELU", "GELU"][act]))
+    res["variants_train"] = rows
+    return res
 
 
 def screen_queries(n_mats, block=64, sw=3840, sh=2160, seed=SEED_BASE + 40):
@@ -453,7 +562,59 @@ def cpu_baseline(d, codes, wts, budget_s=15.0):
     cores = os.cpu_count()
     return {"value": n / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{n} area-uniform random texels of the 4096^2 9ch chain, oracle decode_texels "
-                      f"(C fp64, OpenMP {cores} threads), {el:.2f} s"}
+                      f"(C fp64, OpenMP {cores} threads), {el:.2f} s",
+            "protocol": oracle_protocol(O)}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _oracle_codes(O, d, seed):
+    grids = []
+    for j in range(O.num_levels(d)):
+        r0, r1 = O.grid_res(d, j)
+        grids += [(r0 * r0 * d.c0, d.b0), (r1 * r1 * d.c1, d.b1)]
+    return gen_codes(seed, grids)
+
+
+def oracle_protocol(O):
+    """SURVEY.md 8(d) oracle timing: the CPU model, C1 (256^2 x 8ch mip 0) on ONE core, the full
+    C2 chain (2048^2 x 9ch, 5,592,405 texels) and one C4 training step (4 x 256^2 crops at LOD 0
+    of the 4096^2 9ch material: loss + every gradient) on all host cores.  Reported only."""
+    out = {"cpu_model": _cpu_model(), "cores": os.cpu_count()}
+    d1 = Profile.named("ntc0.2", 256, 8)
+    c1, w1 = _oracle_codes(O, d1, SEED_BASE + 0), gen_weights_f16(SEED_BASE + 1, d1.input_dim, 8)
+    t0 = time.perf_counter()
+    O.decode_mip(d1, c1, w1, 0, nthreads=1)
+    out["C1_single_core_s"] = round(time.perf_counter() - t0, 3)
+    d2 = Profile.named("ntc0.2", 2048, 9)
+    c2, w2 = _oracle_codes(O, d2, SEED_BASE + 1), gen_weights_f16(SEED_BASE + 2, d2.input_dim, 9)
+    t0 = time.perf_counter()
+    for m in range(O.num_mips(2048)):
+        O.decode_mip(d2, c2, w2, m, nthreads=os.cpu_count())
+    el = time.perf_counter() - t0
+    out["C2_full_chain_s"] = round(el, 3)
+    out["C2_Gtexel_s"] = round(5592405 / el / 1e9, 6)
+    d4 = Profile.named("ntc0.2", W, C)
+    NL = sum(r0 * r0 * d4.c0 + r1 * r1 * d4.c1 for r0, r1 in (O.grid_res(d4, j) for j in range(O.num_levels(d4))))
+    lat = gen_latents(SEED_BASE + 6, NL)
+    par = gen_weights_f32(SEED_BASE + 7, d4.input_dim, C)
+    ref = u8_to_f16_bits(gen_reference_u8(SEED_BASE + 4, W, C))
+    crops = gen_crops(SEED_BASE + 3, W, 0, 4, 256)
+    t0 = time.perf_counter()
+    O.train_grads(d4, lat, par, 0, crops, ref, 7, 1, nthreads=os.cpu_count())
+    el = time.perf_counter() - t0
+    out["C4_step_s"] = round(el, 3)
+    out["C4_texels_s"] = round(4 * 256 * 256 / el, 1)
+    return out
 
 
 def run_reference(args, rank, world):

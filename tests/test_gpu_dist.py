@@ -154,7 +154,7 @@ def test_sharded_dp_matches_single_process(world, mip, crop):
     latents and the weights equal single-process training on the same global batches (fp32
     summation order only), and the ranks agree.  At mips 3-4 every crop spans several bands,
     so boxes that different readers send back to one owner overlap (their halo-gradient adds
-    must not race: ADVICE r1)."""
+    must not race: ADVICE r1).  Latents: see the bound below."""
     from paper_2305_17105_b200.synth import gen_crops
 
     steps = 3
@@ -187,7 +187,14 @@ def test_sharded_dp_matches_single_process(world, mip, crop):
     for _, l, p, full in res:
         assert np.allclose(l, losses, rtol=1e-5)
         assert np.allclose(p, ref_par, rtol=1e-4, atol=1e-6)
-        assert np.allclose(full, ref_lat, rtol=1e-4, atol=1e-6)
+        # The two runs sum the same fp32 gradient contributions in different orders (ranks,
+        # atomics); from step 2 on the 1-ulp weight differences can flip fp16 activation
+        # roundings, and Adam normalises whatever gradient difference results.  A lost or
+        # doubled halo contribution moves a latent by O(lr_latent) per step (Adam's update
+        # size), reordering by ~1e-5 (measured: <= 8e-6 over 3 steps at mip 4): the bound
+        # 2e-3 * lr_latent * steps separates the two by > 100x.
+        atol = 2e-3 * 0.01 * steps
+        assert np.abs(full - ref_lat).max() <= atol, np.abs(full - ref_lat).max()
     for r in res[1:]:
         assert np.array_equal(res[0][2], r[2]) and np.array_equal(res[0][3], r[3])
 
