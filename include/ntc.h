@@ -184,8 +184,9 @@ typedef struct {
 } ntc_train_buffers;
 
 /* One batch = n_crops crops at one mip: crops host int32 [n_crops][4] =
- * (x0, y0, w, h), each inside the mip; ref device fp16 reference mip image,
- * row y at ref + y*ref_row_stride_elems (R24).  n_crops <= NTC_MAX_CROPS.
+ * (x0, y0, w, h), each inside the mip; ref device fp16 reference mip image, 4-byte
+ * aligned (else NTC_ERR_INVALID_ARGUMENT), row y at ref + y*ref_row_stride_elems (R24).
+ * n_crops <= NTC_MAX_CROPS.
  * norm_texels: the B of the mean over B*c values (R17); 0 = this batch's own texel count.
  * A data-parallel rank passes the global batch's count so that the sum of the ranks'
  * gradients is the global gradient.                                                     */

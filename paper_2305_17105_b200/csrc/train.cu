@@ -54,9 +54,10 @@ struct TrainParams {
     const __half* noisy;
     float* grad_lat;
     const uint8_t* wimg;  // fp16 weight image (TrainSmem layout, WEND bytes)
-    float* partial;     // [grid][P]
+    float* partial;     // [grid][Pst]
     float* loss_partial;  // [grid * slots]
     int32_t P;
+    int32_t Pst;          // partial stride: P rounded up to 4 floats (16-byte stores)
     int32_t freeze;       // frozen phase: no latent gradients
 };
 
@@ -132,17 +133,53 @@ __device__ __forceinline__ void box_locate(const Box* box, const int32_t* start,
     li = B.off + ((int64_t)yy * B.r + B.x0) * B.C + rem;
 }
 
+#ifdef NTC_TRAIN_TRACE
+// phase timestamps of the MMA-issuing thread of every slot (tools/trace_train.py only; the
+// product library is built without NTC_TRAIN_TRACE): [cta][slot][iteration < 16][warp][32] clocks;
+// k < 16 after a phase boundary, 16 + k when the warp arrives at the barrier that ends phase k
+__device__ uint32_t* g_trace;
+extern "C" void ntc_trace_set(uint32_t* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof p); }
+#define NTC_TRACE(k)                                                                                          \
+    do {                                                                                                     \
+        if (lane == 0 && g_trace && iter < 16)                                                               \
+            g_trace[((((size_t)blockIdx.x * SLOTS + slot) * 16 + iter) * 8 + (warp & 7)) * 32 + (k)] =         \
+                (uint32_t)clock64();                                                                         \
+    } while (0)
+__device__ __forceinline__ uint32_t gtimer_lo() {
+    uint32_t t;
+    asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
+    return t;
+}
+// kernel-level stamps in iteration slot 15: 0 entry, 1 after the prologue, 2 after the tile
+// loop, 3 exit (clock64); 4 entry, 5 exit (%globaltimer, ns)
+#define NTC_TRACE_K(k, v)                                                                                     \
+    do {                                                                                                     \
+        if (lane == 0 && g_trace)                                                                            \
+            g_trace[((((size_t)blockIdx.x * SLOTS + (warp >> 3)) * 16 + 15) * 8 + (warp & 7)) * 32 + (k)] = (v); \
+    } while (0)
+#else
+#define NTC_TRACE_K(k, v) \
+    do {                  \
+    } while (0)
+#define NTC_TRACE(k) \
+    do {             \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------------ fused forward + backward
 // SMEM layout for depth HM (1: [D,64,64,c]; 2: [D,64,64,64,c], R11) and KA 64-column K atoms
 // of X (1: K1 = 64, NTC 0.2; 2: K1 = 80/96, the other Table 2 profiles): fp16 weight images
-// (W1 in KA atoms with b1 at column D, W2, [W2b], W3 with 16 rows) + fp32 biases b2[64],
-// [b2b[64]], b3[16]; then per tile pipeline ("slot") the SW128 activation tiles.  Only the
-// depth-1 K1 = 64 layout leaves SMEM for two slots.
+// (W1 in KA atoms with b1 at column D, W2, [W2b], W3 with 16 rows), a constant ones tile and the
+// bias atoms of b2, [b2b], b3 (SW32 K = 16 tiles: the biases enter the accumulators as one extra
+// K = 16 MMA of ones x bias, so no epilogue adds them); then per tile pipeline ("slot") the
+// SW128 activation tiles.  Only the depth-1 K1 = 64 layout leaves SMEM for two slots.
 template <int HM, int KA = 1>
 struct TrainSmemT {
-    static constexpr uint32_t W1 = 0, W2 = 8192u * KA, W2B = W2 + 8192, W3 = W2 + 8192u * HM, BIAS = W3 + 2048;
-    static constexpr uint32_t NBIAS = 64 * HM + 16;
-    static constexpr uint32_t WEND = ((BIAS + 4 * NBIAS + 1023) / 1024) * 1024;
+    static constexpr uint32_t W1 = 0, W2 = 8192u * KA, W2B = W2 + 8192, W3 = W2 + 8192u * HM;
+    static constexpr uint32_t ONES = W3 + 2048;   // [128][16] fp16 SW32, column 0 = 1
+    static constexpr uint32_t B2A = ONES + 4096;  // [64][16] SW32, column 0 = b2 (then b2b)
+    static constexpr uint32_t B3A = B2A + 2048u * HM;  // [16][16] SW32, column 0 = b3
+    static constexpr uint32_t WEND = ((B3A + 512 + 1023) / 1024) * 1024;
     static constexpr uint32_t TILE = 128 * 128;  // one 128 x 64 fp16 SW128 tile
     // depth 1: X[KA] H1 H2 G1 G2 D3; depth 2: X[KA] H1 H2 H3 G1 G2 G3 D3
     // (G1 and G2 adjacent: [delta1 | delta2] is one N=128 operand of the weight-gradient MMA)
@@ -154,6 +191,7 @@ struct TrainSmemT {
     static constexpr uint32_t WG_BYTES = NT * TILE;
     static constexpr uint32_t MISC = 256 + 16 * NTC_MAX_CROPS + 4 * (NTC_MAX_CROPS + 1) + 4 * NTC_MAX_CROPS + 12;
     static constexpr uint32_t BYTES = 1024 + WEND + SLOTS * WG_BYTES + MISC;
+    static_assert(BYTES <= 232448, "training SMEM layout exceeds 227 KB");
 };
 using TrainSmem = TrainSmemT<1>;
 constexpr uint32_t TRAIN_WEND_MAX = TrainSmemT<2, 2>::WEND;
@@ -161,6 +199,16 @@ constexpr uint32_t TRAIN_WEND_MAX = TrainSmemT<2, 2>::WEND;
 __device__ __forceinline__ void sts_row_chunk(uint32_t tile, int row, int chunk, uint32_t a, uint32_t b, uint32_t c,
                                               uint32_t d) {
     sts128(tile + (uint32_t)row * 128u + ((uint32_t)(chunk ^ (row & 7)) << 4), a, b, c, d);
+}
+
+// byte offset of element (row, k < 16) in a K-major SW32 tile (rows of 32 B, 8-row atoms of
+// 256 B; the 16-byte chunk index is XORed with bit 2 of the row)
+__host__ __device__ constexpr uint32_t sw32_offset(uint32_t row, uint32_t k) {
+    return row * 32u + ((((k >> 3) & 1u) ^ ((row >> 2) & 1u)) << 4) + (k & 7u) * 2u;
+}
+
+__device__ __forceinline__ uint64_t umma_desc_k_sw32(uint32_t saddr) {
+    return umma_desc(saddr, 16, 256, UMMA_SWIZZLE_32B);
 }
 
 __device__ __forceinline__ uint4 lds_row_chunk(uint32_t tile, int row, int chunk) {
@@ -190,47 +238,53 @@ __device__ __forceinline__ void red_add_v2(float* p, float a, float b) {
 
 __device__ __forceinline__ uint32_t h2u(float a, float b) { return pack_half2(a, b); }
 
-// fp16 SW128 weight image of the current fp32 master weights (t3): W1 (+ b1 at column D, it
-// multiplies X's constant 1), W2, [W2b], W3 (16 rows); the hidden and output biases as fp32
-// values of their fp16 rounding (R14), added in the epilogues.  ABI parameter order: W1, b1,
-// W2, b2, [W2b, b2b], W3, b3.
-__host__ __device__ constexpr int wimg_items(int hm, int ka) { return (1 + ka + hm) * 4096 + 64 * hm + 16; }
+// fp16 weight image of the current fp32 master weights (t3), the SMEM layout copied verbatim:
+// W1 (+ b1 at column D, it multiplies X's constant 1), W2, [W2b], W3 (16 rows) as SW128
+// K-major atoms; the ones tile and the bias atoms b2, [b2b], b3 (column 0, SW32) -- the biases
+// take their fp16 rounding like every weight (R14).  ABI parameter order: W1, b1, W2, b2,
+// [W2b, b2b], W3, b3.  One item = one fp16 element.
+__host__ __device__ constexpr int wimg_items(int hm, int ka) {
+    return (ka + hm) * 4096 + 1024 + 2048 + 1024 * hm + 256;
+}
 template <int HM, int KA>
 __device__ __forceinline__ void train_wimg_item_t(int i, const float* __restrict__ w, int D, int c,
                                                   uint8_t* __restrict__ img) {
     using S = TrainSmemT<HM, KA>;
     if (i >= wimg_items(HM, KA)) return;
-    const int P1 = D * HID;                  // b1
+    const int P1 = D * HID;                            // b1
     const int o3 = P1 + HID + HM * (HID * HID + HID);  // W3
-    float* bias = reinterpret_cast<float*>(img + S::BIAS);
-    if (i >= (1 + KA + HM) * 4096) {
-        const int j = i - (1 + KA + HM) * 4096;
-        if (j < 64 * HM) {  // hidden biases b2 (, b2b)
-            const int l = j / 64, o = j % 64;
-            bias[j] = __half2float(__float2half_rn(w[P1 + HID + l * (HID * HID + HID) + HID * HID + o]));
-        } else {            // b3 (16 slots, c used)
-            const int o = j - 64 * HM;
-            bias[j] = o < c ? __half2float(__float2half_rn(w[o3 + HID * c + o])) : 0.0f;
-        }
-        return;
-    }
-    const int part = i / 4096, e = i % 4096, r = e / 64, kk = e % 64;
     float v = 0.0f;
-    uint32_t base;
-    if (part < KA) {  // W1 atom `part`: X features 64 part + kk
-        const int k = 64 * part + kk;
-        v = k < D ? w[r * D + k] : (k == D ? w[P1 + r] : 0.0f);
-        base = S::W1 + 8192u * part;
-    } else if (part < KA + HM) {  // hidden matrix
-        const int l = part - KA;
-        v = w[P1 + HID + l * (HID * HID + HID) + r * HID + kk];
-        base = l == 0 ? S::W2 : S::W2B;
-    } else {
-        if (r >= 16) return;
+    uint32_t off;
+    if (i < (KA + HM) * 4096) {
+        const int part = i / 4096, e = i % 4096, r = e / 64, kk = e % 64;
+        if (part < KA) {  // W1 atom `part`: X features 64 part + kk
+            const int k = 64 * part + kk;
+            v = k < D ? w[r * D + k] : (k == D ? w[P1 + r] : 0.0f);
+            off = S::W1 + 8192u * part + sw128_offset(r, kk);
+        } else {          // hidden matrix l
+            const int l = part - KA;
+            v = w[P1 + HID + l * (HID * HID + HID) + r * HID + kk];
+            off = (l == 0 ? S::W2 : S::W2B) + sw128_offset(r, kk);
+        }
+    } else if ((i -= (KA + HM) * 4096) < 1024) {  // W3, 16 rows (c used)
+        const int r = i / 64, kk = i % 64;
         v = r < c ? w[o3 + r * HID + kk] : 0.0f;
-        base = S::W3;
+        off = S::W3 + sw128_offset(r, kk);
+    } else if ((i -= 1024) < 2048) {  // ones tile: column 0 = 1
+        const int r = i / 16, kk = i % 16;
+        v = kk == 0 ? 1.0f : 0.0f;
+        off = S::ONES + sw32_offset(r, kk);
+    } else if ((i -= 2048) < 1024 * HM) {  // hidden bias atoms: row j column 0 = b2[j] (b2b)
+        const int l = i / 1024, r = (i % 1024) / 16, kk = i % 16;
+        v = kk == 0 ? w[P1 + HID + l * (HID * HID + HID) + HID * HID + r] : 0.0f;
+        off = S::B2A + 2048u * l + sw32_offset(r, kk);
+    } else {  // b3 atom (16 rows, c used)
+        i -= 1024 * HM;
+        const int r = i / 16, kk = i % 16;
+        v = (kk == 0 && r < c) ? w[o3 + HID * c + r] : 0.0f;
+        off = S::B3A + sw32_offset(r, kk);
     }
-    *reinterpret_cast<__half*>(img + base + sw128_offset(r, kk)) = __float2half_rn(v);
+    *reinterpret_cast<__half*>(img + off) = __float2half_rn(v);
 }
 
 // t2: noisy = latent + U(-Q/2, Q/2) (one draw per latent per step), grad = 0, over the footprint
@@ -349,7 +403,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::WEND + SLOTS * S::WG_BYTES);
-    float* s_loss = reinterpret_cast<float*>(s_bar + 2 * SLOTS);
+    float* s_loss = reinterpret_cast<float*>(s_bar + 2 * SLOTS + 2);  // after the weight-copy barrier
     uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_loss + 4);
     uint32_t* s_tmem = s_pe + 32;
     int4* s_crop = reinterpret_cast<int4*>(s_tmem + 4);
@@ -357,15 +411,25 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     int* s_csh = s_ts + NTC_MAX_CROPS + 1;  // log2 of the crop width when it is a power of 2, else -1
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    NTC_TRACE_K(0, (uint32_t)clock64());
+#ifdef NTC_TRAIN_TRACE
+    NTC_TRACE_K(4, gtimer_lo());
+#endif
     // slot and the TMEM base go through a shuffle: provably warp-uniform, so the MMA-issuing
     // thread keeps its descriptors in uniform registers (no R2UR waterfall per tcgen05.mma)
     const int slot = __shfl_sync(0xffffffffu, warp >> 3, 0), h = (warp >> 2) & 1, q = warp & 3, row = q * 32 + lane;
     const int c = CT ? CT : p.c;
 
-    // ---- weight images (fp16, SW128 K-major, built once per step by the trailing blocks of
-    // prep_kernel); the same images serve the backward MMAs through MN-major descriptors
-    for (uint32_t i = tid; i < S::WEND / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.wimg) + i);
+    // ---- weight images (fp16, built once per step by the trailing blocks of prep_kernel; the
+    // same images serve the backward MMAs through MN-major descriptors): one bulk TMA copy,
+    // waited by the MMA-issuing threads only, after the first tile's loads are in flight
+    uint64_t* s_wbar = s_bar + 2 * SLOTS;
+    if (tid == 0) {
+        mbar_init(s_wbar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(s_wbar, S::WEND);
+        bulk_g2s(smem_u32(smem), p.wimg, S::WEND, s_wbar);
+    }
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
     if (tid < 4) s_loss[tid] = 0.0f;
     if (tid < NTC_MAX_CROPS) {
@@ -386,6 +450,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    NTC_TRACE_K(1, (uint32_t)clock64());
 
     // TMEM per slot: depth 1: [0,128) dW-a accumulator, [128,144) dW-b, [192,256) scratch;
     // depth 2: [0,128) dW-a, [128,192) dW-m (the middle layer), [192,208) dW-b, [256,320) scratch
@@ -417,7 +482,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     };
     const uint64_t dW1 = umma_desc_k_sw128(sbase + S::W1), dW2 = umma_desc_k_sw128(sbase + S::W2);
     const uint64_t dW3 = umma_desc_k_sw128(sbase + S::W3), dW2B = umma_desc_k_sw128(sbase + S::W2B);
-    const float* s_bias = reinterpret_cast<const float*>(smem + S::BIAS);  // b2[64], [b2b[64]], b3[16]
+    // bias MMAs: ones[128 x 16] x bias atom^T adds b2 / b2b / b3 to every row of the accumulator
+    const uint64_t dONES = umma_desc_k_sw32(sbase + S::ONES), dB2 = umma_desc_k_sw32(sbase + S::B2A);
+    const uint64_t dB2B = umma_desc_k_sw32(sbase + S::B2A + 2048), dB3 = umma_desc_k_sw32(sbase + S::B3A);
     const uint64_t dX = umma_desc_k_sw128(tX), dH1 = umma_desc_k_sw128(tH1), dH2 = umma_desc_k_sw128(tH2);
     const uint64_t dG1 = umma_desc_k_sw128(tG1), dG2 = umma_desc_k_sw128(tG2), dD3 = umma_desc_k_sw128(tD3);
     const uint64_t dHL = umma_desc_k_sw128(tHL), dG3 = umma_desc_k_sw128(tG3);
@@ -433,6 +500,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
     constexpr uint32_t ID64_BT = idesc_f16(128, 64, false, true), IDX_BT = idesc_f16(128, NLATP, false, true);
     constexpr uint32_t ID64_AB = idesc_f16(128, 64, true, true), ID16_AB = idesc_f16(128, 16, true, true);
+    constexpr uint32_t ID128_AB = idesc_f16(128, 128, true, true);
 
     float loss_acc = 0.0f;
     bool first = true;
@@ -487,10 +555,14 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     // reference texel, half 1 the four fp16 G1 cells (4 x C1 halves); one register array
     // serves both halves
     constexpr int NVW = 2 * (C0 > C1 ? C0 : C1);  // 32-bit words: 4 cells x C/2
+    constexpr int NRW = ((CT ? CT : 16) * 2 + 2 + 3) / 4;  // reference window words (<= 9)
     struct Fetch {
         Texel t;
         uint32_t v[NVW];   // h = 0: G0 taps (tap-major, 2 C0 words); h = 1: G1 taps (2 C1 words)
-        uint32_t ref[8];   // h = 0: reference channels (fp16 pairs)
+        // h = 0: the reference texel's c fp16 values as raw 32-bit words of the aligned window
+        // around them, shifted into channel pairs only at the loss (loads stay in flight)
+        uint32_t ref[NRW];
+        uint32_t rsh;      // 16 when the texel starts 2 bytes into a word, else 0
     };
     // one fp16 cell of C channels (C/2 words) with the widest aligned vector loads
     auto load_cell_h = [&](const __half* cell, int C, uint32_t* out) {
@@ -521,13 +593,19 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
 #pragma unroll
             for (int t = 0; t < 4; ++t) load_cell_h(g0 + (ty[t >> 1] * p.r0 + tx[t & 1]) * C0, C0, f.v + t * (C0 / 2));
             const uint16_t* rp = p.ref + (int64_t)f.t.y * p.ref_stride + (int64_t)f.t.x * c;
+            // the texel's 2c bytes as aligned words: full 32-bit words while they end inside the
+            // texel, the last half word as a 16-bit load (no byte past the texel is read)
+            const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(rp) & 2u);
+            const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(rp) & ~uintptr_t(3));
+            const int nb = 2 * c + (int)sh;  // window bytes
 #pragma unroll
-            for (int o = 0; o < 8; ++o) {
-                uint16_t lo = 0, hi = 0;
-                if (2 * o < c) lo = __ldg(rp + 2 * o);
-                if (2 * o + 1 < c) hi = __ldg(rp + 2 * o + 1);
-                f.ref[o] = (uint32_t)lo | ((uint32_t)hi << 16);
+            for (int k = 0; k < NRW; ++k) {
+                uint32_t v = 0u;
+                if (4 * k + 4 <= nb) v = __ldg(wp + k);
+                else if (4 * k + 2 == nb) v = __ldg(reinterpret_cast<const uint16_t*>(wp + k));
+                f.ref[k] = v;
             }
+            f.rsh = sh * 8u;
         } else {
             int tx[2], ty[2];
             uint32_t ax, ay;
@@ -541,13 +619,24 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     int tile = blockIdx.x * SLOTS + slot;
     const int tstride = gridDim.x * SLOTS;
     Fetch F;
+#ifdef NTC_SLOT1_DELAY  // desynchronisation experiment (tools/trace_train.py only)
+    if (slot == 1) {
+        const long long t0 = clock64();
+        while (clock64() - t0 < NTC_SLOT1_DELAY) {
+        }
+    }
+#endif
     if (tile < p.n_tiles) fetch(tile, F);
-    for (; tile < p.n_tiles; tile += tstride) {
+    if (issuer) mbar_wait(s_wbar, 0);  // the weight images have landed (async proxy -> MMA reads)
+    int iter = 0;
+    for (; tile < p.n_tiles; tile += tstride, ++iter) {
+        NTC_TRACE(0);
         const Texel T = F.t;
         const bool valid = T.valid;
-        uint32_t rawref[8];
+        uint32_t rawref[8];  // channel pairs (2o, 2o + 1) of the reference texel
 #pragma unroll
-        for (int o = 0; o < 8; ++o) rawref[o] = F.ref[o];
+        for (int o = 0; o < 8; ++o)
+            rawref[o] = o < NRW ? __funnelshift_r(F.ref[o], o + 1 < NRW ? F.ref[o + 1] : 0u, F.rsh) : 0u;
         // ---- a2-a4: this half's part of the X row (canonical order, R4) -> SW128 tile(s): half 0
         // the G0 words [0, 2 C0), half 1 the G1 bilinear, PE, LOD + bias one and the padding up
         // to K1; both parts start on a 16-byte chunk (2 C0 is a multiple of 4 words)
@@ -605,7 +694,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                 }
             }
         }
+        NTC_TRACE(17);
         sync_slot();
+        NTC_TRACE(1);
         // ---- t3: forward.  Z1 = X W1^T (+b1)
         if (issuer) {
             tc_fence_after();
@@ -617,9 +708,10 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         }
         if (tile + tstride < p.n_tiles) fetch(tile + tstride, F);  // next tile's loads in flight
         wait_mma();
+        NTC_TRACE(2);
         // two 16-column tcgen05.ld per half, the second in flight while the first is processed
         // (the register-dependent wait orders the uses after it)
-        auto hidden_epilogue = [&](uint32_t tH, uint32_t tG, const float* bias) {
+        auto hidden_epilogue = [&](uint32_t tH, uint32_t tG) {
             uint32_t r[2][16];
             tmem_ld16(t_s + lane_off + 32 * h, r[0]);
             tmem_wait_ld_r16(r[0]);
@@ -630,13 +722,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                 uint32_t hv[8], gv[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    float z0 = __uint_as_float(r[part][2 * i]), z1 = __uint_as_float(r[part][2 * i + 1]);
-                    if (bias) {
-                        const float2 zb = __fadd2_rn(
-                            make_float2(z0, z1), *reinterpret_cast<const float2*>(bias + 32 * h + 16 * part + 2 * i));
-                        z0 = zb.x;
-                        z1 = zb.y;
-                    }
+                    const float z0 = __uint_as_float(r[part][2 * i]), z1 = __uint_as_float(r[part][2 * i + 1]);
                     if constexpr (ACT == 0) {
                         hgelu_and_grad2(z0, z1, hv[i], gv[i]);
                     } else {
@@ -655,37 +741,46 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                 }
             }
         };
-        hidden_epilogue(tH1, tG1, nullptr);
+        hidden_epilogue(tH1, tG1);
+        NTC_TRACE(19);
         sync_slot();
+        NTC_TRACE(3);
         // Z2 = H1 W2^T + b2
         if (issuer) {
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH1 + 2 * kk, dW2 + 2 * kk, ID64, kk > 0);
+            mma_f16_ss(t_s, dONES, dB2, ID64, 1);
             mma_commit(bar);
         }
         wait_mma();
-        hidden_epilogue(tH2, tG2, s_bias);
+        NTC_TRACE(4);
+        hidden_epilogue(tH2, tG2);
         if constexpr (HM == 2) {  // Z3 = H2 W2b^T + b2b
             sync_slot();
             if (issuer) {
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH2 + 2 * kk, dW2B + 2 * kk, ID64, kk > 0);
+                mma_f16_ss(t_s, dONES, dB2B, ID64, 1);
                 mma_commit(bar);
             }
             wait_mma();
-            hidden_epilogue(tH3, tG3, s_bias + 64);
+            hidden_epilogue(tH3, tG3);
         }
+        NTC_TRACE(21);
         sync_slot();
+        NTC_TRACE(5);
         // Y = H_last W3^T + b3
         if (issuer) {
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dHL + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
+            mma_f16_ss(t_s, dONES, dB3, ID16, 1);
             mma_commit(bar);
         }
         wait_mma();
+        NTC_TRACE(6);
         // ---- t4: mean-L2 loss (R17) on half 0 (it holds the reference); delta3 = 2 (y - R)
         // fed unscaled, 1/(B c) applied in fp32
         if (h == 0) {
@@ -696,7 +791,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
 #pragma unroll
             for (int o = 0; o < 16; ++o) {
                 const float rf = __half2float(__ushort_as_half((uint16_t)(rawref[o >> 1] >> (16 * (o & 1)))));
-                const float e = (valid && o < c) ? __uint_as_float(r[o]) + s_bias[64 * HM + o] - rf : 0.0f;
+                const float e = (valid && o < c) ? __uint_as_float(r[o]) - rf : 0.0f;
                 loss_acc = fmaf(e, e, loss_acc);
                 d3[o] = 2.0f * e;
             }
@@ -704,7 +799,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             sts_row_chunk(tD3, row, 1, h2u(d3[8], d3[9]), h2u(d3[10], d3[11]), h2u(d3[12], d3[13]),
                           h2u(d3[14], d3[15]));
         }
+        NTC_TRACE(23);
         sync_slot();
+        NTC_TRACE(7);
         // ---- t5: dH_last = d3 W3
         if (issuer) {
             tc_fence_after();
@@ -712,6 +809,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             mma_commit(bar);
         }
         wait_mma();
+        NTC_TRACE(8);
         auto delta_epilogue = [&](uint32_t tG) {  // delta = fp16(dH) * hardGELU'(Z), in place
             uint32_t r[2][16];
             tmem_ld16(t_s + lane_off + 32 * h, r[0]);
@@ -751,7 +849,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             wait_mma();
             delta_epilogue(tG2);
         }
+        NTC_TRACE(25);
         sync_slot();
+        NTC_TRACE(9);
         // dH1 = d2 W2
         if (issuer) {
             tc_fence_after();
@@ -761,8 +861,11 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             mma_commit(bar);
         }
         wait_mma();
+        NTC_TRACE(10);
         delta_epilogue(tG1);  // G1 tile now holds delta1
+        NTC_TRACE(27);
         sync_slot();
+        NTC_TRACE(11);
         // dX = d1 W1 (latent columns) ; weight gradients accumulated in TMEM
         if (issuer) {
             tc_fence_after();
@@ -782,19 +885,29 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                     mma_f16_ss(t_acc_m, mXH2 + (uint64_t)(kk * 128), mG3 + (uint64_t)(kk * 128), ID64_AB,
                                (!first || kk > 0) ? 1u : 0u);
             }
+            if constexpr (KA == 1) {
+                // dW1/db1 and dW2/db2 in one N = 128 MMA per K step: [X^T; H1^T] [delta1 | delta2]
+                // (adjacent tiles; the diagonal blocks are used, rows 64-127 of the delta1 half
+                // and rows < 64 of the delta2 half except the constant row are not)
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-                mma_f16_ss(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
-                           (!first || kk > 0) ? 1u : 0u);
-            // dW1/db1: [X^T; H1^T] delta1 (K1 = 64: rows 64-127 unused) or [X0^T; X1^T] delta1
-            const uint64_t mA1 = KA == 1 ? mXH1 : mXX;
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_f16_ss(t_acc_a, mXH1 + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID128_AB,
+                               (!first || kk > 0) ? 1u : 0u);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-                mma_f16_ss(t_acc_a, mA1 + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID64_AB,
-                           (!first || kk > 0) ? 1u : 0u);
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_f16_ss(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
+                               (!first || kk > 0) ? 1u : 0u);
+                // dW1/db1: [X0^T; X1^T] delta1
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_f16_ss(t_acc_a, mXX + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID64_AB,
+                               (!first || kk > 0) ? 1u : 0u);
+            }
             mma_commit(bar2);
         }
         wait_mma();
+        NTC_TRACE(12);
         first = false;
         pending_w = true;
         // ---- t7: latent-gradient scatter: half 0 the G0 taps (unweighted), half 1 the G1 taps
@@ -907,102 +1020,75 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                 }
             }
         }
+        NTC_TRACE(15);
         tc_fence_before();
     }
 
+    NTC_TRACE_K(2, (uint32_t)clock64());
     if (pending_w) {
         mbar_wait(bar2, phase2);
         phase2 ^= 1;
         tc_fence_after();
     }
-    // ---- t6: the CTA's weight-gradient partial (unscaled, one per CTA, fixed order): slot 1
-    // (depth 1) parks its TMEM accumulators in the (now idle) SMEM tile area, slot 0 adds its
-    // own and writes the partial.  Half 0 handles the dW1/db1 columns [0, 64) (and the middle
-    // layer's dW2b/db2b at depth 2), half 1 the dW2/db2 columns [64, 128) and dW3/db3.
-    float* part = p.partial + (size_t)blockIdx.x * p.P;
-    float* park = reinterpret_cast<float*>(smem + S::WEND) + row * 145;  // [128][144] (+1 pad)
-    constexpr int NV = HM == 1 ? 80 : 128;
-    auto read_acc = [&](float (&v)[NV], bool have) {
-#pragma unroll
-        for (int blk = 0; blk < 2; ++blk) {
-            uint32_t r[32];
-            tmem_ld32(t_acc_a + lane_off + 64 * h + 32 * blk, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[32 * blk + e] = have ? __uint_as_float(r[e]) : 0.0f;
-        }
-        if (h == 1) {
-            uint32_t r[16];
-            tmem_ld16(t_acc_b + lane_off, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int o = 0; o < 16; ++o) v[64 + o] = have ? __uint_as_float(r[o]) : 0.0f;
-        } else if (HM == 2) {
+    NTC_TRACE_K(6, (uint32_t)clock64());
+    // ---- t6: the CTA's weight-gradient partial (unscaled, one per CTA, fixed order).  Each
+    // slot writes its TMEM accumulators into its own (now idle) tile area in ABI order -- every
+    // accumulator (row, column) used maps to one ABI index, and consecutive rows (lanes) to
+    // consecutive addresses -- then all threads add the slots' buffers and store the partial
+    // with coalesced 16-byte stores.  Half 0 handles the dW1/db1 columns [0, 64) (and the
+    // middle layer's dW2b/db2b at depth 2), half 1 the dW2/db2 columns [64, 128) and dW3/db3.
+    {
+        const bool have = !first;  // a slot without tiles never wrote its accumulators
+        const int m = row;         // stacked rows: X features (64 per atom), then H units at [64,128)
+        const int P1 = D * HID, o2 = P1 + HID, o2b = o2 + HID * HID + HID, o3 = P1 + HID + HM * (HID * HID + HID);
+        float* buf = reinterpret_cast<float*>(smem + S::WEND + (uint32_t)slot * S::WG_BYTES);
+        // 64 accumulator columns at t -> buf[base + col * stride] (base < 0: row unused)
+        auto put64 = [&](uint32_t t, int base, int stride) {
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) {
                 uint32_t r[32];
-                tmem_ld32(t_acc_m + lane_off + 32 * blk, r);
+                tmem_ld32(t + lane_off + 32 * blk, r);
                 tmem_wait_ld();
+                if (base >= 0) {
 #pragma unroll
-                for (int e = 0; e < 32; ++e) v[NV - 64 + 32 * blk + e] = have ? __uint_as_float(r[e]) : 0.0f;
-            }
-        }
-    };
-    __syncthreads();  // every slot is done with its tiles before the area is reused
-    if (SLOTS == 2 && slot == 1) {
-        float v[NV];
-        read_acc(v, !first);
-#pragma unroll
-        for (int e = 0; e < 64; ++e) park[64 * h + e] = v[e];
-        if (h == 1) {
-#pragma unroll
-            for (int o = 0; o < 16; ++o) park[128 + o] = v[64 + o];
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (slot == 0) {
-        float v[NV];
-        read_acc(v, !first);
-        if (SLOTS == 2) {
-#pragma unroll
-            for (int e = 0; e < 64; ++e) v[e] += park[64 * h + e];
-            if (h == 1) {
-#pragma unroll
-                for (int o = 0; o < 16; ++o) v[64 + o] += park[128 + o];
-            }
-        }
-        // ABI offsets: W1, b1, W2, b2, [W2b, b2b], W3, b3
-        const int P1 = D * HID, o2 = P1 + HID, o2b = o2 + HID * HID + HID, o3 = P1 + HID + HM * (HID * HID + HID);
-        const int m = row;  // stacked rows: X features (64 per atom), then H units at [64,128)
-        if (h == 0) {
-#pragma unroll
-            for (int col = 0; col < 64; ++col) {
-                if (m < D) part[col * D + m] = v[col];       // dW1[j][i]
-                else if (m == D) part[P1 + col] = v[col];    // db1[j]
-            }
-            if constexpr (HM == 2) {
-#pragma unroll
-                for (int col = 0; col < 64; ++col) {
-                    if (m == DX) part[o2b + HID * HID + col] = v[64 + col];           // db2b[j]
-                    else if (m >= 64) part[o2b + col * HID + (m - 64)] = v[64 + col];  // dW2b[j][i]
+                    for (int e = 0; e < 32; ++e) buf[base + (32 * blk + e) * stride] = have ? __uint_as_float(r[e]) : 0.0f;
                 }
             }
+        };
+        sync_slot();  // the slot's tiles are free (its last weight-gradient MMAs were waited above)
+        if (h == 0) {
+            put64(t_acc_a, m < D ? m : (m == D ? P1 : -1), m < D ? D : 1);  // dW1[j][i], db1[j]
+            if constexpr (HM == 2)
+                put64(t_acc_m, m >= 64 ? o2b + (m - 64) : (m == DX ? o2b + HID * HID : -1), m >= 64 ? HID : 1);
         } else {
+            put64(t_acc_a + 64, m >= 64 ? o2 + (m - 64) : (m == DX ? o2 + HID * HID : -1), m >= 64 ? HID : 1);
+            uint32_t r[16];
+            tmem_ld16(t_acc_b + lane_off, r);
+            tmem_wait_ld();
+            const int base = m >= 64 ? o3 + (m - 64) : (m == DX ? o3 + HID * c : -1), stride = m >= 64 ? HID : 1;
+            if (base >= 0) {
 #pragma unroll
-            for (int col = 0; col < 64; ++col) {
-                if (m == DX) part[o2 + HID * HID + col] = v[col];           // db2[j]
-                else if (m >= 64) part[o2 + col * HID + (m - 64)] = v[col];  // dW2[j][i]
-            }
-#pragma unroll
-            for (int o = 0; o < 16; ++o) {
-                if (o >= c) continue;
-                if (m == DX) part[o3 + HID * c + o] = v[64 + o];               // db3[o]
-                else if (m >= 64) part[o3 + o * HID + (m - 64)] = v[64 + o];   // dW3[o][i]
+                for (int o = 0; o < 16; ++o)
+                    if (o < c) buf[base + o * stride] = have ? __uint_as_float(r[o]) : 0.0f;  // dW3[o][i], db3[o]
             }
         }
+        __syncthreads();
+        const float4* b0 = reinterpret_cast<const float4*>(smem + S::WEND);
+        const float4* b1 = reinterpret_cast<const float4*>(smem + S::WEND + S::WG_BYTES);
+        float4* part = reinterpret_cast<float4*>(p.partial + (size_t)blockIdx.x * p.Pst);
+        for (int i = tid; i < p.Pst / 4; i += blockDim.x) {
+            float4 v = b0[i];
+            if constexpr (SLOTS == 2) {
+                const float4 u = b1[i];
+                v.x += u.x;
+                v.y += u.y;
+                v.z += u.z;
+                v.w += u.w;
+            }
+            part[i] = v;  // entries [P, Pst) are never read
+        }
     }
+    NTC_TRACE_K(10, (uint32_t)clock64());
     {
         float v = loss_acc;
 #pragma unroll
@@ -1013,6 +1099,10 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     __syncthreads();
     tc_fence_after();
     if (tid < SLOTS) p.loss_partial[blockIdx.x * SLOTS + tid] = s_loss[tid];
+    NTC_TRACE_K(3, (uint32_t)clock64());
+#ifdef NTC_TRAIN_TRACE
+    NTC_TRACE_K(5, gtimer_lo());
+#endif
     if (warp == 0) tmem_dealloc(*s_tmem, 512);
 }
 
@@ -1287,7 +1377,7 @@ extern "C" ntc_status ntc_trainer_create(const ntc_desc* d, ntc_trainer** out) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t P = ntc_num_params(d);
-    cudaError_t e = cudaMalloc(&t->partial, sizeof(float) * P * t->num_sms);
+    cudaError_t e = cudaMalloc(&t->partial, sizeof(float) * ((P + 3) & ~3) * t->num_sms);
     if (e == cudaSuccess) e = cudaMalloc(&t->loss_partial, sizeof(float) * t->num_sms * TrainSmemT<1>::SLOTS);
     if (e == cudaSuccess) e = cudaMalloc(&t->wimg, TRAIN_WEND_MAX);
     if (e == cudaSuccess) e = cudaMemset(t->wimg, 0, TRAIN_WEND_MAX);
@@ -1561,6 +1651,8 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
     if (flags & NTC_STEP_GRADS) {
         if (!buf->latents || !buf->noisy || !buf->grad_lat || !buf->params || !buf->grad_par || !loss || !batch->ref)
             return api_fail(NTC_ERR_INVALID_ARGUMENT, "NULL buffer");
+        if (reinterpret_cast<uintptr_t>(batch->ref) & 3)  // read as aligned 32-bit words
+            return api_fail(NTC_ERR_INVALID_ARGUMENT, "reference image must be 4-byte aligned");
         // t2: noisy latents + zeroed gradients over the footprint
         PrepParams pp;
         memset(&pp, 0, sizeof pp);
@@ -1633,6 +1725,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         tp.partial = t->partial;
         tp.loss_partial = t->loss_partial;
         tp.P = (int32_t)P;
+        tp.Pst = (int32_t)((P + 3) & ~3);
         tp.freeze = hp->freeze_latents;
         int slots = 1;
         uint32_t smem_bytes = 0;
@@ -1656,7 +1749,7 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
             k<<<grid, slots * 256, smem_bytes, st>>>(tp);
             // t6: deterministic cross-CTA reduction, scaled by 1/(B c); with APPLY in the same
             // call, t8 rides in the same launch (weights Adam'd as they are reduced)
-            const ReduceArgs ra{t->partial,  (size_t)P,  t->loss_partial, grid, (int)P, grid * slots,
+            const ReduceArgs ra{t->partial,  (size_t)tp.Pst,  t->loss_partial, grid, (int)P, grid * slots,
                                 tp.inv_bc,   buf->grad_par, loss,         status};
             const int rblocks = (int)((P + 31) / 32);
             if ((flags & NTC_STEP_APPLY) && apply_buffers_ok(buf)) {
