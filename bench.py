@@ -10,9 +10,14 @@ One step = one pass of the hot path over synthetic inputs resident in HBM:
             of a 4096^2 9-channel material (configs[3]), when the library provides it.
 L2 is flushed (256 MiB write) before every timed step, outside the CUDA-event window.
 Extra lines at N=1 (--no-extras skips them): `random` = configs[2]'s 2^24 random-access
-queries on a 4096^2 16-channel material; `multi` = the Table 4 screen workload over 8 materials (f3).
-Multi-GPU (torchrun): weak scaling, one independent material per rank (configs[4]:
-decode needs no collective); time = max over ranks of the device time.
+queries on a 4096^2 16-channel material; `multi` = the Table 4 screen workload over 8 materials
+(f3); `configs` = the other SURVEY.md 8(d) rows (C1, C2, C3a, stress, C4 LOD mix, variants).
+`c5` at every N (--no-c5 skips it): configs[4], 64 materials -- material-parallel decode and
+training, and at N > 1 the stacked data-parallel trainer (one all-reduce for all materials).
+Multi-GPU (torchrun): weak scaling, one independent material per rank for the headline decode
+(no collective), the sharded data-parallel training step (stratified crops, plus a
+`train_uniform` line with the R19 placement whose halos cross bands) and a `comm` record (backend,
+NCCL version, all-reduce of ones = rank count); time = max over ranks of the device time.
 """
 from __future__ import annotations
 
@@ -281,6 +286,12 @@ def run_ours(args, rank, world, local_rank):
                                              "train", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")}}}
     # e2e through the public API from pinned host buffers (rank 0 and every rank alike)
     res["e2e"] = e2e(args, ntc, torch, d, codes, wts, dev, world)
+    if world > 1:
+        res["comm"] = comm_check(torch, dist, dev, world)
+        if train is not None:
+            res["train_uniform"] = bench_train_uniform(args, ntc, torch, dev, flush, d, train, world)
+    if not args.no_c5:
+        res["c5"] = bench_c5(args, ntc, torch, dev, flush, rank, world)
     if world == 1 and not args.no_extras:
         res["random"] = bench_random(args, ntc, torch, dev, flush)
         res["multi"] = bench_multi(args, ntc, torch, dev, flush)
@@ -431,6 +442,243 @@ def bench_configs(args, ntc, torch, dev, flush):
         rows.append(_row(dv, 4 * 256 * 256, train_time(dv, b, SEED_BASE + 11), train_flops_per_texel(dv), peak,
                          profile=name, hidden_mats=hm, activation=["hardGELU", "GELU"][act]))
     res["variants_train"] = rows
+    return res
+
+
+def _device_codes(ntc, torch, d, seed, dev):
+    """iid uniform codes of every grid (the synth.gen_codes recipe), drawn on the device from
+    a seeded generator: 64 materials x 12.3 M codes are set up in milliseconds."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    parts = [torch.randint(0, 1 << b, (n,), generator=g, device=dev, dtype=torch.uint8)
+             for n, b in ntc.grid_list(d)]
+    return torch.cat(parts)
+
+
+def _device_latents(ntc, torch, d, seed, dev):
+    """U(-0.2, 0.2) fp32 training latents (the synth.gen_latents recipe), seeded, on the device."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    return torch.rand(ntc.ntc_num_latents(d), generator=g, device=dev) * 0.4 - 0.2
+
+
+def comm_check(torch, dist, dev, world):
+    """The process group the N > 1 numbers ran on: backend, NCCL version, and an all-reduce of
+    ones that must sum to the world size (the rank count, measured)."""
+    t = torch.ones(1, device=dev)
+    dist.all_reduce(t)
+    out = {"backend": dist.get_backend(), "world": world, "allreduce_of_ones": float(t.item())}
+    try:
+        v = torch.cuda.nccl.version()
+        out["nccl_version"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    except Exception:
+        out["nccl_version"] = None
+    return out
+
+
+def bench_train_uniform(args, ntc, torch, dev, flush, d, train, world):
+    """The sharded data-parallel step on the compression workload's own batches: per step a
+    LOD from the paper's law (R26) and 4 x N crops of min(256, w_m)^2 placed
+    uniformly over that mip (R19), each owned by the rank whose band holds its origin -- crops
+    straddle bands (always at the coarser mips), so the halo all-to-alls carry latents and
+    gradients (the main N > 1 line draws LOD-0 crops inside each band, stratified)."""
+    import torch.distributed as dist
+
+    from paper_2305_17105_b200.compress import sample_lod
+    from paper_2305_17105_b200.dist import ShardedDataParallelTrainer
+
+    dp = ShardedDataParallelTrainer(d, train["tb"]["latents"], train["tb"]["params"])
+    M = ntc.ntc_num_mips(d)
+    chain = [train["ref"].view(torch.float16).reshape(W, W, C)]  # box-filtered fp16 mips
+    while chain[-1].shape[0] > 1:
+        a = chain[-1].float()
+        chain.append((0.25 * (a[0::2, 0::2] + a[1::2, 0::2] + a[0::2, 1::2] + a[1::2, 1::2])).half())
+    chain = [c.reshape(-1).view(torch.int16) for c in chain]
+    reps = max(3, min(args.steps, 10))
+    rng = np.random.default_rng(SEED_BASE + 91)
+    steps = []
+    for i in range(reps + 1):
+        m = sample_lod(rng, M)
+        crops = gen_crops(SEED_BASE + 90 + i, W, m, 4 * world, 256)
+        steps.append((m, crops, dp.plan(m, crops)))
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tot, halo, texels = 0.0, 0, 0
+    for i, (m, crops, plan) in enumerate(steps):
+        flush.zero_()
+        dist.barrier()
+        e0.record(s)
+        dp.step(m, crops, chain[m], (W >> m) * C, ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, i + 1, 7, 1, 0),
+                plan=plan)
+        e1.record(s)
+        e1.synchronize()
+        if i > 0:
+            tot += e0.elapsed_time(e1) / 1e3
+            halo += sum(plan.recv_sizes)
+            texels += int((crops[:, 2] * crops[:, 3]).sum())
+    t = torch.tensor([tot, float(halo)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"value": texels / float(t[0].item()), "unit": "texel/s", "ms_per_step": float(t[0].item()) / reps * 1e3,
+            "parallelism": f"data-parallel x{world}, latents sharded by row bands; per step a LOD from the paper's "
+                           "law and 4 x N crops uniform over that mip (R19, R26), owner-assigned: halo all-to-alls of "
+                           "latents and gradients",
+            "lods": [m for m, _, _ in steps[1:]], "halo_latents_received_per_step_max_rank": int(t[1].item()) // reps}
+
+
+def _device_reference_f16(torch, seed, width, channels, dev):
+    """synth.gen_reference_u8's recipe (rank-3 mix of 3 smooth fields + 10% noise, unorm8) on
+    the device, then R = fp16(v / 255) (R24): the field parameters come from the same seeded
+    numpy stream, the per-texel noise from a seeded device generator."""
+    rng = np.random.default_rng(seed)
+    y = torch.arange(width, device=dev, dtype=torch.float32)[:, None] / width
+    x = torch.arange(width, device=dev, dtype=torch.float32)[None, :] / width
+    fields = []
+    for _ in range(3):
+        f = torch.zeros((width, width), device=dev)
+        for o in range(4):
+            fr = 2.0 ** (o + 1)
+            for _ in range(2):
+                a = rng.uniform(0, 2 * np.pi, 4).astype(np.float32)
+                k = rng.uniform(0.5, 1.5, 2).astype(np.float32) * fr
+                f += (torch.sin(2 * np.pi * float(k[0]) * x + float(a[0])) *
+                      torch.cos(2 * np.pi * float(k[1]) * y + float(a[1]))) / (o + 1)
+        f -= f.min()
+        f /= max(float(f.max()), 1e-6)
+        fields.append(f)
+    mix = rng.uniform(0.0, 1.0, size=(3, channels)).astype(np.float32)
+    mix /= mix.sum(0, keepdims=True)
+    img = torch.stack(fields, -1) @ torch.from_numpy(mix).to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    img = 0.9 * img + 0.1 * torch.rand(img.shape, generator=g, device=dev)
+    u8 = torch.clamp(torch.round(img * 255.0), 0, 255)
+    return (u8.double() / 255.0).half().view(torch.int16).reshape(-1)
+
+
+def bench_c5(args, ntc, torch, dev, flush, rank, world):
+    """configs[4] (C5): 64 materials of 4096^2 x 9ch NTC 0.2 (per-material seed = base +
+    material id), SURVEY.md 8(e):
+      decode   material-parallel: rank r decodes the full chains of materials r, r+N, ...
+               (no collective) into a ring of two output buffers;
+      train_mp material-parallel training: one GRADS|APPLY step (4 x 256^2 crops at LOD 0) of
+               each of the rank's materials, no collective;
+      train_dp (N > 1) data-parallel over texel batches of all 64 materials at once: latents
+               sharded by row bands per material, one batched halo all-to-all each way and ONE
+               all-reduce of the stacked [dW | loss] of the 64 materials (2.2 MB) per step.
+    Every number: texels of all ranks / max over ranks of the device time (weak scaling)."""
+    import torch.distributed as dist
+
+    M = args.c5_materials
+    d = Profile.named("ntc0.2", W, C)
+    T = ntc.ntc_chain_texels(d)
+    mine = list(range(rank, M, world))
+    reps = max(3, min(args.steps, 5))
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        fn()  # warm-up
+        tot = 0.0
+        for _ in range(reps):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            e0.record(s)
+            fn()
+            e1.record(s)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1) / 1e3
+        t = tot / reps
+        if world > 1:
+            tt = torch.tensor([t], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    pk, _ = _peaks()
+    peak = pk["bf16_tflops"]
+    res = {"workload": f"configs[4]: {M} materials of 4096^2 x 9ch NTC0.2", "materials": M, "n_gpus": world}
+    # decode: the rank's share of full chains
+    mats = [ntc.Material(d, _device_codes(ntc, torch, d, SEED_BASE + 4 + k, dev),
+                         torch.from_numpy(gen_weights_f16(SEED_BASE + 5 + k, d.input_dim, C).view(np.int16)).to(dev))
+            for k in mine]
+    ring = [torch.empty((T * C,), dtype=torch.float16, device=dev) for _ in range(2)]
+
+    def decode_all():
+        for i, m in enumerate(mats):
+            ntc.ntc_decode_chain(m, ring[i & 1])
+
+    t = timed(decode_all)
+    tf = decode_flops_per_texel(d) * T * len(mine) / t / 1e12
+    res["decode"] = {"value": M * T / t / 1e9, "unit": UNIT, "ms_per_step": t * 1e3,
+                     "parallelism": f"material-parallel x{world}: {len(mine)} chains per rank, no collective",
+                     "roofline": {"bound": "tensor", "achieved": round(tf, 2), "peak": peak, "unit": "TFLOP/s",
+                                  "frac": round(tf / peak, 4)}}
+    del mats, ring
+    # training state for the rank's materials (material-parallel)
+    refs = {}  # material k's synthetic reference (mip 0), generated on the device
+
+    def ref(k):
+        if k not in refs:
+            refs[k] = _device_reference_f16(torch, SEED_BASE + 60 + k, W, C, dev)
+        return refs[k]
+
+    def state(k):
+        NL, P = ntc.ntc_num_latents(d), ntc.ntc_num_params(d)
+        tb = {n: torch.zeros(NL, device=dev) for n in ("m_lat", "v_lat", "grad_lat", "noisy")}
+        tb.update({n: torch.zeros(P, device=dev) for n in ("m_par", "v_par", "grad_par")})
+        tb["latents"] = _device_latents(ntc, torch, d, SEED_BASE + 6 + k, dev)
+        tb["params"] = torch.from_numpy(gen_weights_f32(SEED_BASE + 7 + k, d.input_dim, C)).to(dev)
+        return tb
+
+    B = 4 * 256 * 256
+    sts = [(k, state(k)) for k in mine]
+    for k in (range(M) if world > 1 else mine):
+        ref(k)
+    tr = ntc.Trainer(d)
+    bufs = [ntc.make_buffers(tb) for _, tb in sts]
+    loss = torch.zeros(1, device=dev)
+    crops = [[gen_crops(SEED_BASE + 3 + 1000 * i + k, W, 0, 4, 256) for k in range(M)] for i in range(reps + 1)]
+    it = [0]
+
+    def train_mp():
+        i = it[0] % len(crops)
+        it[0] += 1
+        for (k, _), b in zip(sts, bufs):
+            ntc.ntc_train_step(tr, b, ntc.make_batch(0, crops[i][k], ref(k), W * C),
+                               ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, it[0], SEED_BASE + k, 1, 0), loss)
+
+    t = timed(train_mp)
+    tf = train_flops_per_texel(d) * B * len(mine) / t / 1e12
+    res["train_mp"] = {"value": M * B / t, "unit": "texel/s", "ms_per_step": t * 1e3,
+                       "parallelism": f"material-parallel x{world}: {len(mine)} materials per rank, no collective",
+                       "workload": f"one GRADS|APPLY step per material, 4 x 256^2 crops at LOD 0 ({M * B} texels)",
+                       "roofline": {"bound": "tensor", "achieved": round(tf, 2), "peak": peak, "unit": "TFLOP/s",
+                                    "frac": round(tf / peak, 4)}}
+    del sts, bufs
+    if world > 1:
+        from paper_2305_17105_b200.dist import StackedDataParallelTrainer, stratified_crops
+
+        all_st = [state(k) for k in range(M)]
+        dp = StackedDataParallelTrainer(d, [tb["latents"] for tb in all_st], [tb["params"] for tb in all_st])
+        rng = np.random.default_rng(SEED_BASE + 77)
+        dcrops = [[stratified_crops(d, 0, world, 4, 256, rng) for _ in range(M)] for _ in range(reps + 1)]
+        plans = [dp.plan(0, c) for c in dcrops]
+        j = [0]
+
+        def train_dp():
+            i = j[0] % len(dcrops)
+            j[0] += 1
+            dp.step(0, dcrops[i], [ref(k) for k in range(M)], W * C,
+                    ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, j[0], SEED_BASE, 1, 0), plan=plans[i])
+
+        t = timed(train_dp)
+        res["train_dp"] = {"value": M * B * world / t, "unit": "texel/s", "ms_per_step": t * 1e3,
+                           "parallelism": f"data-parallel x{world} over texel batches of all {M} materials: latents "
+                                          "sharded by row bands, batched halo all-to-alls, one stacked all-reduce "
+                                          f"of {M} x [dW | loss] ({M * (ntc.ntc_num_params(d) + 1) * 4} B)",
+                           "workload": f"per step and rank: 4 x 256^2 crops per material in the rank's band",
+                           "gpu_launches_per_step": dp.launches}
     return res
 
 
@@ -657,6 +905,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-extras", action="store_true", help="skip the random-access and multi-material lines")
+    ap.add_argument("--no-c5", action="store_true", help="skip the 64-material configs[4] lines")
+    ap.add_argument("--c5-materials", type=int, default=64, help="materials of the configs[4] lines (64)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -355,3 +355,119 @@ class ShardedDataParallelTrainer:
             if s != self.rank:
                 ntc_boxes_copy(d, band_boxes(d, N, s), recv[s], out, NTC_BOX_UNPACK)
         return out
+
+
+# ------------------------------------------------------------------ several materials (C5)
+def stacked_segments(plans):
+    """Layout of the batched halo exchange of several materials (C5): the
+    piece a rank sends to peer t is [material 0 -> t | material 1 -> t | ...].  Returns
+    (send_sizes[t], recv_sizes[t], send_off[k][t], recv_off[k][t]) where the offsets are
+    positions inside the concatenated send / receive buffers (peer-major, then material)."""
+    M = len(plans)
+    world = len(plans[0].send_sizes) if M else 0
+    send_sizes = [sum(p.send_sizes[t] for p in plans) for t in range(world)]
+    recv_sizes = [sum(p.recv_sizes[t] for p in plans) for t in range(world)]
+    send_off = [[0] * world for _ in range(M)]
+    recv_off = [[0] * world for _ in range(M)]
+    s = r = 0
+    for t in range(world):
+        for k in range(M):
+            send_off[k][t], recv_off[k][t] = s, r
+            s += plans[k].send_sizes[t]
+            r += plans[k].recv_sizes[t]
+    return send_sizes, recv_sizes, send_off, recv_off
+
+
+class StackedDataParallelTrainer:
+    """Several materials (C5: 64 x 4096^2) trained data-parallel over texel batches with the
+    latent grids of every material sharded by row bands (ShardedDataParallelTrainer's
+    scheme).  One step covers every material: ONE all-to-all carries all materials' halo
+    latents, ONE the halo gradients back, and ONE all-reduce the stacked [dW | loss] of all
+    materials ([M][P + 1] fp32: 64 x 33.8 KB = 2.2 MB at C5); owners then
+    apply Adam to their bands.  Collectives per step: 3, independent of M."""
+
+    def __init__(self, d, latents_list, params_list, group=None):
+        import torch.distributed as dist
+
+        self.d, self.group, self.dist = d, group, dist
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.M = len(latents_list)
+        dev = latents_list[0].device
+        self.dev = dev
+        self.P = ntc_num_params(d)
+        self.stack = torch.zeros((self.M, self.P + 1), device=dev)  # [dW | loss] per material
+        self.mats = []
+        for k in range(self.M):
+            tr = ShardedDataParallelTrainer(d, latents_list[k], params_list[k], group)
+            tr.flat = self.stack[k]  # rows of the stacked all-reduce buffer
+            tr.t["grad_par"] = tr.flat[: self.P]
+            tr.bufs = make_buffers(tr.t)
+            self.mats.append(tr)
+        self._sbuf = torch.empty(0, device=dev)
+        self._rbuf = torch.empty(0, device=dev)
+        self.launches = 0
+
+    def plan(self, mip: int, crops_list):
+        """Per-material StepPlans and the batched exchange layout (host only, ahead of time)."""
+        plans = [m.plan(mip, c) for m, c in zip(self.mats, crops_list)]
+        return plans, stacked_segments(plans)
+
+    def _buffers(self, ns, nr):
+        if self._sbuf.numel() < ns:
+            self._sbuf = torch.empty(ns, device=self.dev)
+        if self._rbuf.numel() < nr:
+            self._rbuf = torch.empty(nr, device=self.dev)
+        return self._sbuf[:ns], self._rbuf[:nr]
+
+    def step(self, mip: int, crops_list, refs, ref_stride: int, hp: Hparams, plan=None):
+        """crops_list[k]: material k's global crop list; refs[k]: its reference mip image."""
+        plans, (ssz, rsz, soff, roff) = plan if plan is not None else self.plan(mip, crops_list)
+        self.launches = 0
+        sbuf, rbuf = self._buffers(sum(ssz), sum(rsz))
+        any_halo = any(p.any_halo for p in plans)
+        # 1. every material's halo latents in one all-to-all
+        if any_halo:
+            for k, (m, pl) in enumerate(zip(self.mats, plans)):
+                for t in range(self.world):
+                    if pl.send_sizes[t]:
+                        m._copy(pl.send_boxes[t], m.t["latents"], sbuf[soff[k][t]: soff[k][t] + pl.send_sizes[t]],
+                                NTC_BOX_PACK)
+            self.mats[0]._exchange(sbuf, ssz, rbuf, rsz)
+            for k, (m, pl) in enumerate(zip(self.mats, plans)):
+                for t in range(self.world):
+                    if pl.recv_sizes[t]:
+                        m._copy(pl.recv_boxes[t], rbuf[roff[k][t]: roff[k][t] + pl.recv_sizes[t]], m.t["latents"],
+                                NTC_BOX_UNPACK)
+        # 2. GRADS of every material on this rank's crops (rows of the stacked buffer)
+        for m, pl, ref in zip(self.mats, plans, refs):
+            m._copy(pl.mine_g, None, m.t["grad_lat"], NTC_BOX_ZERO)
+            loss = m.flat[self.P: self.P + 1]
+            if pl.mine.shape[0] > 0:
+                mb = make_batch(pl.mip, pl.mine, ref, ref_stride, norm_texels=pl.norm)
+                ntc_train_step(m.trainer, m.bufs, mb, hp, loss, flags=NTC_STEP_GRADS)
+                m.launches += 3
+            else:
+                m.flat.zero_()
+        # 3. every material's halo gradients back to their owners in one all-to-all
+        if any_halo:
+            for k, (m, pl) in enumerate(zip(self.mats, plans)):
+                for t in range(self.world):
+                    if pl.recv_sizes[t]:
+                        m._copy(pl.recv_boxes[t], m.t["grad_lat"], rbuf[roff[k][t]: roff[k][t] + pl.recv_sizes[t]],
+                                NTC_BOX_PACK)
+            self.mats[0]._exchange(rbuf, rsz, sbuf, ssz)
+            for k, (m, pl) in enumerate(zip(self.mats, plans)):
+                for t in range(self.world):
+                    if pl.send_sizes[t]:
+                        m._copy(pl.send_boxes[t], sbuf[soff[k][t]: soff[k][t] + pl.send_sizes[t]], m.t["grad_lat"],
+                                NTC_BOX_ADD)
+        # 4. one all-reduce of the stacked [dW | loss]; 5. owners apply Adam per material
+        self.dist.all_reduce(self.stack, group=self.group)
+        for m, pl in zip(self.mats, plans):
+            ntc_train_apply_boxes(m.trainer, m.bufs, pl.mine_g, hp)
+            m.launches += 1
+        self.launches = sum(m.launches for m in self.mats)
+        return self.stack[:, self.P]
+
+    def gather_latents(self, k: int) -> torch.Tensor:
+        return self.mats[k].gather_latents()

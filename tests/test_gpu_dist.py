@@ -210,7 +210,7 @@ def test_bench_two_ranks_json_line():
     env = dict(os.environ, NTC_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-extras"]
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-extras", "--c5-materials", "4"]
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -221,3 +221,81 @@ def test_bench_two_ranks_json_line():
         assert k in r, k
     assert r["n_gpus"] == 2 and r["scaling"] == "weak" and r["value"] > 0
     assert "sharded" in r["train"]["parallelism"]
+    assert r["comm"]["world"] == 2 and r["comm"]["allreduce_of_ones"] == 2.0
+    assert r["train_uniform"]["halo_latents_received_per_step_max_rank"] > 0  # R19 crops cross bands
+    c5 = r["c5"]
+    assert c5["materials"] == 4 and c5["decode"]["value"] > 0 and c5["train_mp"]["value"] > 0
+    assert c5["train_dp"]["value"] > 0 and "stacked all-reduce" in c5["train_dp"]["parallelism"]
+
+
+def _stacked_worker(rank, world, port, q, steps, mip, crop, M):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2305_17105_b200 as ntc
+        from paper_2305_17105_b200.dist import StackedDataParallelTrainer
+        from paper_2305_17105_b200.synth import gen_crops, gen_latents, gen_weights_f32
+
+        d, _, _, ref = _setup_chain()
+        NL = ntc.ntc_num_latents(d)
+        lats = [torch.from_numpy(gen_latents(100 + k, NL)).to(DEV) for k in range(M)]
+        pars = [torch.from_numpy(gen_weights_f32(200 + k, d.input_dim, 8)).to(DEV) for k in range(M)]
+        tr = StackedDataParallelTrainer(d, lats, pars)
+        refd = torch.from_numpy(ref[mip].view(np.int16)).to(DEV)
+        losses = []
+        for s in range(steps):
+            hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, s + 1, 7, 1, 0)
+            crops = [gen_crops(40 + 10 * k + s, 128, mip, 6, crop) for k in range(M)]
+            losses.append(tr.step(mip, crops, [refd] * M, (128 >> mip) * 8, hp).cpu().numpy().copy())
+        full = [tr.gather_latents(k).cpu().numpy().copy() for k in range(M)]
+        pars_out = [tr.mats[k].t["params"].cpu().numpy().copy() for k in range(M)]
+        torch.cuda.synchronize()
+        q.put((rank, np.array(losses), pars_out, full, tr.launches))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,mip,crop", [(2, 0, 32), (3, 3, 12)])
+def test_stacked_materials_match_single_process(world, mip, crop):
+    """C5's stacked data-parallel trainer (several materials, latents sharded by row bands,
+    one batched halo all-to-all each way and ONE all-reduce of every material's [dW | loss])
+    equals training each material alone on the same global batches."""
+    from paper_2305_17105_b200.synth import gen_crops, gen_latents, gen_weights_f32
+
+    M, steps = 3, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stacked_worker, args=(r, world, port, q, steps, mip, crop, M))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    d, _, _, ref = _setup_chain()
+    NL, P = ntc.ntc_num_latents(d), ntc.ntc_num_params(d)
+    refd = torch.from_numpy(ref[mip].view(np.int16)).to(DEV)
+    for k in range(M):
+        t = {n: torch.zeros(NL, device=DEV) for n in ("m_lat", "v_lat", "grad_lat", "noisy")}
+        t.update({n: torch.zeros(P, device=DEV) for n in ("m_par", "v_par", "grad_par")})
+        t["latents"] = torch.from_numpy(gen_latents(100 + k, NL)).to(DEV)
+        t["params"] = torch.from_numpy(gen_weights_f32(200 + k, d.input_dim, 8)).to(DEV)
+        tr, bufs, loss = ntc.Trainer(d), ntc.make_buffers(t), torch.zeros(1, device=DEV)
+        losses = []
+        for s in range(steps):
+            hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, s + 1, 7, 1, 0)
+            crops = gen_crops(40 + 10 * k + s, 128, mip, 6, crop)
+            ntc.ntc_train_step(tr, bufs, ntc.make_batch(mip, crops, refd, (128 >> mip) * 8), hp, loss)
+            losses.append(float(loss.item()))
+        torch.cuda.synchronize()
+        for _, l, p, full, _ in res:
+            assert np.allclose(l[:, k], losses, rtol=1e-5)
+            assert np.allclose(p[k], t["params"].cpu().numpy(), rtol=1e-4, atol=1e-6)
+            # latent bound: see test_sharded_dp_matches_single_process
+            assert np.abs(full[k] - t["latents"].cpu().numpy()).max() <= 2e-3 * 0.01 * steps

@@ -3,7 +3,8 @@ product code).  Like sass_lines.py, but every instruction is attributed to the O
 the given source file in its inline chain (`nvdisasm -gi`), so inlined helpers and lambdas count
 at their call site in the kernel body.
 
-usage: sass_regions.py SASS.csv CUBIN FUNCTION_MANGLED FILE 'name:lo-hi,name:lo-hi,...'"""
+usage: sass_regions.py SASS.csv CUBIN FUNCTION_MANGLED FILE 'name:lo-hi,name:lo-hi,...' [--innermost]
+(--innermost: attribute to the innermost line of FILE instead, for kernels built of lambdas)"""
 import collections
 import csv
 import re
@@ -14,28 +15,36 @@ LINE = re.compile(r'//## File "([^"]+)", line (\d+)(.*)')
 INL = re.compile(r'inlined at "([^"]+)", line (\d+)')
 
 
-def outer_map(cubin, fn, fname):
+def outer_map(cubin, fn, fname, innermost=False):
+    """instruction index -> line of `fname` (outermost, or innermost) of the longest inline
+    chain among the line comments nvdisasm prints before that instruction"""
     txt = subprocess.run(["nvdisasm", "-gi", cubin], capture_output=True, text=True).stdout
-    out, inside, cur = [], False, None
+    out, inside, best, last = [], False, None, None
     for ln in txt.splitlines():
         if ln.startswith(".text."):
             inside = ln.strip() == f".text.{fn}:"
+            best = None
             continue
         if not inside:
             continue
         m = LINE.search(ln)
         if m:
             chain = [(m.group(1), int(m.group(2)))] + [(f, int(l)) for f, l in INL.findall(m.group(3))]
-            hits = [l for f, l in chain if f.endswith(fname)]
-            cur = hits[-1] if hits else None
+            if best is None or len(chain) > len(best):
+                best = chain
             continue
         if re.match(r"\s+/\*[0-9a-f]{4,}\*/\s+[^.]", ln) and "/*" in ln:
-            out.append(cur)
+            if best is not None:  # line entries are sticky: no comment = the previous line
+                last = best
+            hits = [l for f, l in (last or []) if f.endswith(fname)]
+            out.append((hits[0] if innermost else hits[-1]) if hits else None)
+            best = None
     return out
 
 
 def main():
     csvp, cubin, fn, fname, spec = sys.argv[1:6]
+    innermost = "--innermost" in sys.argv
     regions = []
     for item in spec.split(","):
         nm, rng = item.split(":")
@@ -45,7 +54,7 @@ def main():
     hdr = rows[1]
     ix = {h: i for i, h in enumerate(hdr)}
     body = [r for r in rows[2:] if len(r) == len(hdr)]
-    lm = outer_map(cubin, fn, fname)
+    lm = outer_map(cubin, fn, fname, innermost)
     if len(lm) != len(body):
         print(f"warning: {len(lm)} disassembled vs {len(body)} profiled instructions", file=sys.stderr)
     samp, inst = collections.Counter(), collections.Counter()
