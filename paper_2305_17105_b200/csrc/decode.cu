@@ -23,13 +23,21 @@
 
 namespace ntc {
 
-// store NW half2 words of row `row` into a K-major SW128 tile of 128 rows
+// store NW half2 words of row `row` into the A tile of 128 rows: K columns [0, 64) in a
+// K-major SW128 atom, the rest (K1 = 80 / 96) in a K-major SW32 / SW64 part right after it
 template <int NW>
 __device__ __forceinline__ void store_row(uint32_t tile, int row, const uint32_t* w) {
+    constexpr int K2B = NW * 4 - 128;  // bytes per row of the second part (0, 32 or 64)
 #pragma unroll
     for (int c = 0; c < NW / 4; ++c) {
-        const uint32_t addr = tile + (uint32_t)(c >> 3) * (128u * 128u) + (uint32_t)row * 128u +
-                              ((uint32_t)((c & 7) ^ (row & 7)) << 4);
+        uint32_t addr;
+        if (c < 8) {
+            addr = tile + (uint32_t)row * 128u + ((uint32_t)(c ^ (row & 7)) << 4);
+        } else {
+            const uint32_t j = (uint32_t)(c - 8);
+            const uint32_t sw = K2B == 32 ? ((row >> 2) & 1) : ((row >> 1) & 3);
+            addr = tile + 128u * 128u + (uint32_t)row * K2B + ((j ^ sw) << 4);
+        }
         sts128(addr, w[4 * c + 0], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
     }
 }
@@ -105,17 +113,25 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, i
 #endif
 template <class P, int HM>
 struct DecodeSmem {
-    // warpgroups per CTA x tile contexts per warpgroup (8 contexts x 64 TMEM columns = 512
-    // for K1 = 64; the K1 > 64 profiles' 32 KB A tiles leave SMEM for 4 contexts)
-    static constexpr int NWG = P::K1_ATOMS == 1 ? DECODE_NWG : 2;
-    static constexpr int NC = P::K1_ATOMS == 1 ? 8 / DECODE_NWG : 2;
-    static constexpr uint32_t W1_BYTES = P::K1_ATOMS * 64 * 128;
-    static constexpr uint32_t W2_BYTES = 2 * 64 * 128;  // weights atom + bias atom
+    // K1 > 64 (NTC 0.5 / 1.0 / 2.25): the K columns past 64 live in a K-major SW32 (K1 = 80)
+    // or SW64 (K1 = 96) part of 32 / 64 B per row after the SW128 atom, for the X tiles and W1
+    static constexpr int K2 = P::K1_ATOMS == 2 ? P::K1 - 64 : 0;
+    static constexpr uint32_t K2B = 2 * K2;
+    static_assert(K2 == 0 || K2 == 16 || K2 == 32, "second K part: 16 or 32 columns");
+    // warpgroups per CTA x tile contexts per warpgroup: 8 contexts x 64 TMEM columns = 512
+    // (4 contexts for the K1 > 64 profiles at depth 2, whose SMEM does not fit 8)
+    static constexpr bool FULL = P::K1_ATOMS == 1 || HM == 1;
+    static constexpr int NWG = FULL ? DECODE_NWG : 2;
+    static constexpr int NC = FULL ? 8 / DECODE_NWG : 2;
+    static constexpr uint32_t W1_BYTES = 64 * 128 + 64 * K2B;
+    static constexpr uint32_t W2_BYTES = 64 * 128 + 64 * 32;  // SW128 weights + SW32 bias atom
     static constexpr uint32_t W3_BYTES = 2 * 16 * 128;
     static constexpr uint32_t WIMG = W1_BYTES + HM * W2_BYTES + W3_BYTES;
-    static constexpr uint32_t ONES = 128 * 128;         // constant A tile: column 0 = 1
-    static constexpr uint32_t ABUF = P::K1_ATOMS * 128 * 128;  // one per tile context
+    static constexpr uint32_t ONES = 128 * 32;  // constant SW32 A tile (K = 16): column 0 = 1
+    static constexpr uint32_t ABUF = 128 * 128 + 128 * K2B;  // one per tile context
     static constexpr uint32_t BYTES = 1024 + WIMG + ONES + NWG * NC * ABUF + 128 /*pe*/ + 128 /*bars*/ + 16;
+    static_assert(W1_BYTES % 1024 == 0 && W2_BYTES % 1024 == 0 && ABUF % 1024 == 0, "SW128 atoms 1 KB aligned");
+    static_assert(BYTES <= 232448, "decode SMEM layout exceeds 227 KB");
 };
 
 // The tile range a CTA is working through, with the material it belongs to (uniform).
@@ -274,8 +290,8 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     if (!MULTI)
         for (uint32_t i = tid; i < S::WIMG / 16; i += blockDim.x) reinterpret_cast<uint4*>(s_w)[i] = p.wimg[i];
     for (uint32_t i = tid; i < S::ONES / 16; i += blockDim.x) {
-        const uint32_t r = i >> 3, chunk = i & 7;  // 16-byte chunk `chunk` of row r
-        const bool one = chunk == (r & 7);          // logical chunk 0 lands at physical r&7
+        const uint32_t r = i >> 1, chunk = i & 1;     // 16-byte chunk `chunk` of SW32 row r
+        const bool one = chunk == ((r >> 2) & 1);     // logical chunk 0 lands at physical (r>>2)&1
         reinterpret_cast<uint4*>(s_ones)[i] = make_uint4(one ? 0x3C00u : 0u, 0u, 0u, 0u);
     }
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
@@ -297,7 +313,9 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     const uint32_t w1 = smem_u32(s_w), w2 = w1 + S::W1_BYTES, w3 = w2 + HM * S::W2_BYTES;
     // descriptors advance by (bytes >> 4) in their low 14-bit start-address field
     const uint64_t d_w1 = umma_desc_k_sw128(w1), d_w2 = umma_desc_k_sw128(w2), d_w3 = umma_desc_k_sw128(w3);
-    const uint64_t d_ones = umma_desc_k_sw128(smem_u32(s_ones));
+    const uint64_t d_ones = umma_desc_k_sw32(smem_u32(s_ones));
+    // the K columns past 64 of W1 (K1 > 64): SW32 / SW64 part after W1's SW128 atom
+    const uint64_t d_w1b = S::K2B == 64 ? umma_desc_k_sw64(w1 + 64 * 128) : umma_desc_k_sw32(w1 + 64 * 128);
     // Operand hand-off to the MMA issuer: three warps of the warpgroup only arrive on the
     // context's named barrier (bar.arrive) and move on to the other context; the issuing
     // warp waits (bar.sync) and issues.  One barrier id per context keeps successive phases
@@ -351,9 +369,12 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         if (q == C.iq && lane == 0) {
             tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < P::K1 / 16; ++k)
-                mma_f16_ss(C.tcol, C.adesc + (uint64_t)(((k >> 2) * (128 * 128) + (k & 3) * 32) >> 4),
-                           d_w1 + (uint64_t)(((k >> 2) * (64 * 128) + (k & 3) * 32) >> 4), ID64, k > 0);
+            for (int k = 0; k < 4; ++k) mma_f16_ss(C.tcol, C.adesc + (uint64_t)(k * 2), d_w1 + (uint64_t)(k * 2), ID64, k > 0);
+            if constexpr (S::K2 > 0) {  // K columns 64 .. K1 - 1 from the SW32 / SW64 parts
+                const uint64_t a2 = S::K2B == 64 ? umma_desc_k_sw64(C.abuf + 128 * 128) : umma_desc_k_sw32(C.abuf + 128 * 128);
+#pragma unroll
+                for (int k = 0; k < S::K2 / 16; ++k) mma_f16_ss(C.tcol, a2 + (uint64_t)(k * 2), d_w1b + (uint64_t)(k * 2), ID64, 1);
+            }
             mma_commit(C.bar);
         }
         const int nt = C.tile + stride;
@@ -368,7 +389,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         // pipelined TMEM loads for NTC 0.2 mip tiles (+4.9% on the headline chain); the query
         // and multi-material instantiations measured neutral / -2.4% with them, the two-
         // warpgroup K1 > 64 profiles (255 registers, no spills to remove) about -1.5%
-        epilogue_hidden<ACT, UNI && P::K1_ATOMS == 1>(C.tcol + lane_off, C.abuf, row);
+        epilogue_hidden<ACT, UNI>(C.tcol + lane_off, C.abuf, row);
         fence_proxy_async_smem();
         tc_fence_before();
         handoff(C);
@@ -379,9 +400,9 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
             const uint32_t id = last ? ID16 : ID64;
 #pragma unroll
             for (int k = 0; k < 4; ++k) mma_f16_ss(C.tcol, C.adesc + 2 * k, dl + 2 * k, id, k > 0);
-            // hidden-layer bias: one K=16 MMA against the ones tile; the output bias is
-            // added in the output epilogue (FADD.SAT, free with the clamp)
-            if (!last) mma_f16_ss(C.tcol, d_ones, dl + (uint64_t)((64 * 128) >> 4), id, 1);
+            // hidden-layer bias: one K=16 MMA of the ones tile against the layer's SW32 bias
+            // atom; the output bias is added in the output epilogue (FADD.SAT, free with the clamp)
+            if (!last) mma_f16_ss(C.tcol, d_ones, umma_desc_k_sw32(w2 + layer * S::W2_BYTES + 64 * 128), id, 1);
             mma_commit(C.bar);
         }
     };
@@ -502,28 +523,46 @@ __global__ void debug_assemble_kernel(const __grid_constant__ DecodeParams p) {
     for (int k = 0; k < P::D; ++k) X[canonical_col<P>(k)] = (uint16_t)(w[k >> 1] >> (16 * (k & 1)));
 }
 
-// Weight image (global copy of the SMEM layout): W1 in K1/64 SW128 atoms of 64 rows with
-// the G0 columns permuted like X and b1 at column D; per hidden layer a weights atom and a
-// bias atom (column 0 = b); W3 (16 rows) and its bias atom.
+// Weight image (global copy of the SMEM layout): W1's K columns [0, 64) as one SW128 atom of
+// 64 rows (G0 columns permuted like X, b1 at column D) and, for K1 > 64, the columns past 64
+// as an SW32 / SW64 part; per hidden layer an SW128 weights atom and an SW32 bias atom
+// (column 0 = b); W3 (16 rows) and its bias atom.
+template <class P, int HM>
+__device__ __forceinline__ uint32_t wimg_w1_offset(int r, int k) {
+    using S = DecodeSmem<P, HM>;
+    if (k < 64) return sw128_offset(r, k);
+    return 64 * 128 + (S::K2B == 64 ? sw64_offset(r, k - 64) : sw32_offset(r, k - 64));
+}
+template <class P, int HM>
+constexpr int wimg_items() {
+    return 64 * P::K1 + HM * (64 * 64 + 64 * 16) + 2 * 16 * 64;
+}
 template <class P, int HM>
 __global__ void wimg_kernel(const uint16_t* __restrict__ w, int c, uint8_t* __restrict__ img) {
     using S = DecodeSmem<P, HM>;
-    constexpr int D = P::D, n1 = P::K1_ATOMS * 64 * 64, n2 = 2 * 64 * 64, n3 = 2 * 16 * 64;
+    constexpr int D = P::D, n1 = 64 * P::K1, n2 = 64 * 64 + 64 * 16, n3 = 2 * 16 * 64;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n1 + HM * n2 + n3) return;
     const int P1 = D * HID, P2 = HID * HID;
     uint16_t v = 0;
     uint32_t off;
     if (i < n1) {
-        const int atom = i / 4096, r = (i % 4096) / 64, kk = i % 64, k = atom * 64 + kk;
+        const int r = i / P::K1, k = i % P::K1;
         if (k < D) v = w[r * D + canonical_col<P>(k)];
         else if (k == D) v = w[P1 + r];
-        off = atom * 8192 + sw128_offset(r, kk);
+        off = wimg_w1_offset<P, HM>(r, k);
     } else if (i < n1 + HM * n2) {
-        const int l = (i - n1) / n2, e = (i - n1) % n2, bias = e / 4096, r = (e % 4096) / 64, k = e % 64;
+        const int l = (i - n1) / n2, e = (i - n1) % n2;
         const int base = P1 + HID + l * (P2 + HID);
-        v = bias ? (k == 0 ? w[base + P2 + r] : (uint16_t)0) : w[base + r * HID + k];
-        off = S::W1_BYTES + l * S::W2_BYTES + bias * 8192 + sw128_offset(r, k);
+        if (e < 4096) {
+            const int r = e / 64, k = e % 64;
+            v = w[base + r * HID + k];
+            off = S::W1_BYTES + l * S::W2_BYTES + sw128_offset(r, k);
+        } else {
+            const int r = (e - 4096) / 16, k = (e - 4096) % 16;
+            v = k == 0 ? w[base + P2 + r] : (uint16_t)0;
+            off = S::W1_BYTES + l * S::W2_BYTES + 64 * 128 + sw32_offset(r, k);
+        }
     } else {
         const int e = i - n1 - HM * n2, bias = e / 1024, r = (e % 1024) / 64, k = e % 64;
         const int base = P1 + HID + HM * (P2 + HID);
@@ -578,7 +617,7 @@ cudaError_t build_wimg(int pid, int hm, const uint16_t* w, int c, uint8_t* img, 
     return dispatch(pid, hm, [&](auto pr, auto h) {
         using PP = decltype(pr);
         constexpr int HMv = decltype(h)::value;
-        const int n = PP::K1_ATOMS * 4096 + HMv * 8192 + 2048;
+        const int n = wimg_items<PP, HMv>();
         wimg_kernel<PP, HMv><<<(n + 255) / 256, 256, 0, s>>>(w, c, img);
         return cudaGetLastError();
     });

@@ -178,6 +178,17 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N, bool a_
            ((M >> 4) << 24);
 }
 
+// K-major SW32 / SW64 tiles: rows of 32 / 64 B (16 / 32 fp16), 8-row atoms of 256 / 512 B;
+// the 16-byte chunk index is XORed with row bit 2 (SW32) or row bits 1-2 (SW64)
+__device__ __forceinline__ uint64_t umma_desc_k_sw32(uint32_t saddr) { return umma_desc(saddr, 16, 256, UMMA_SWIZZLE_32B); }
+__device__ __forceinline__ uint64_t umma_desc_k_sw64(uint32_t saddr) { return umma_desc(saddr, 16, 512, UMMA_SWIZZLE_64B); }
+__host__ __device__ constexpr uint32_t sw32_offset(uint32_t row, uint32_t k) {
+    return row * 32u + ((((k >> 3) & 1u) ^ ((row >> 2) & 1u)) << 4) + (k & 7u) * 2u;
+}
+__host__ __device__ constexpr uint32_t sw64_offset(uint32_t row, uint32_t k) {
+    return row * 64u + ((((k >> 3) & 3u) ^ ((row >> 1) & 3u)) << 4) + (k & 7u) * 2u;
+}
+
 // byte offset of element (row, k) in a K-major SW128 tile (rows of 128 B, 1024 B aligned)
 __host__ __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t k) {
     return row * 128u + ((((k >> 3) & 7u) ^ (row & 7u)) << 4) + (k & 7u) * 2u;

@@ -201,16 +201,6 @@ __device__ __forceinline__ void sts_row_chunk(uint32_t tile, int row, int chunk,
     sts128(tile + (uint32_t)row * 128u + ((uint32_t)(chunk ^ (row & 7)) << 4), a, b, c, d);
 }
 
-// byte offset of element (row, k < 16) in a K-major SW32 tile (rows of 32 B, 8-row atoms of
-// 256 B; the 16-byte chunk index is XORed with bit 2 of the row)
-__host__ __device__ constexpr uint32_t sw32_offset(uint32_t row, uint32_t k) {
-    return row * 32u + ((((k >> 3) & 1u) ^ ((row >> 2) & 1u)) << 4) + (k & 7u) * 2u;
-}
-
-__device__ __forceinline__ uint64_t umma_desc_k_sw32(uint32_t saddr) {
-    return umma_desc(saddr, 16, 256, UMMA_SWIZZLE_32B);
-}
-
 __device__ __forceinline__ uint4 lds_row_chunk(uint32_t tile, int row, int chunk) {
     uint4 v;
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
