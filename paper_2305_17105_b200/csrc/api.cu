@@ -392,6 +392,7 @@ static ntc_status launch_tiles(const ntc_material* m, int mip_first, int mip_cou
             break;
         p.lin_tiles = p.tile_start[i + 1];
     }
+    p.tma_tiles = ((uintptr_t)out & 15) == 0 ? p.lin_tiles : 0;
     p.pair_tiles = 0;
     if ((m->d.channels & 1) && ((uintptr_t)out & 3) == 0)
         for (int i = 0; i < mip_count; ++i) {

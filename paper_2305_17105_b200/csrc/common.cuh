@@ -75,6 +75,9 @@ struct DecodeParams {
     // mode 0: tiles < lin_tiles write output row (tile * 128 + row) of `out` (whole-tile mips
     // laid out back to back from out_off 0, rows of w_m * c elements)
     int32_t lin_tiles;
+    // mode 0: tiles < tma_tiles (whole-tile mips, 16-byte aligned `out`) are staged in SMEM and
+    // written by one bulk TMA store per tile (decode.cu, DECODE_TMA_OUT)
+    int32_t tma_tiles;
     float b3[16];                  // output bias, added in the output epilogue
 };
 

@@ -111,6 +111,13 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, i
 #ifndef DECODE_NWG
 #define DECODE_NWG 4
 #endif
+// 1: mip-tile output staged in SMEM and written by one bulk TMA store per tile (K1 = 64
+// profiles, whose SMEM has room for the 8 staging buffers); 0 (default): every thread stores
+// its own row.  A/B on B200 (tools/ab_decode.py, 3 alternating runs): the bulk store path is
+// 3% slower (4K chain c = 9: 29.05 vs 29.97 Gtexel/s; c = 16: 29.17 vs 30.23), so it stays off.
+#ifndef DECODE_TMA_OUT
+#define DECODE_TMA_OUT 0
+#endif
 template <class P, int HM>
 struct DecodeSmem {
     // K1 > 64 (NTC 0.5 / 1.0 / 2.25): the K columns past 64 live in a K-major SW32 (K1 = 80)
@@ -129,7 +136,11 @@ struct DecodeSmem {
     static constexpr uint32_t WIMG = W1_BYTES + HM * W2_BYTES + W3_BYTES;
     static constexpr uint32_t ONES = 128 * 32;  // constant SW32 A tile (K = 16): column 0 = 1
     static constexpr uint32_t ABUF = 128 * 128 + 128 * K2B;  // one per tile context
-    static constexpr uint32_t BYTES = 1024 + WIMG + ONES + NWG * NC * ABUF + 128 /*pe*/ + 128 /*bars*/ + 16;
+    // output staging for the bulk TMA store (tiled mode): 128 rows x c halves per context
+    static constexpr bool TMA_OUT = DECODE_TMA_OUT && P::K1_ATOMS == 1;
+    static constexpr uint32_t STAGE = TMA_OUT ? 128 * 16 * 2 : 0;
+    static constexpr uint32_t BYTES =
+        1024 + WIMG + ONES + NWG * NC * (ABUF + STAGE) + 128 /*pe*/ + 128 /*bars*/ + 16;
     static_assert(W1_BYTES % 1024 == 0 && W2_BYTES % 1024 == 0 && ABUF % 1024 == 0, "SW128 atoms 1 KB aligned");
     static_assert(BYTES <= 232448, "decode SMEM layout exceeds 227 KB");
 };
@@ -259,6 +270,8 @@ struct Ctx {
     int id;             // context index (named barrier selector)
     int iq;             // warp (lane quarter) that issues this context's MMAs
     uint64_t adesc;     // SW128 K-major descriptor of abuf
+    uint32_t stage;     // SMEM output staging (bulk TMA store)
+    int ptile;          // tile whose staged output awaits its bulk store (-1: none)
 };
 
 // CT: the channel count as a compile-time constant (0: the runtime p.c), for the output path;
@@ -272,7 +285,8 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     uint8_t* s_w = smem;
     uint8_t* s_ones = smem + S::WIMG;
     uint8_t* s_a = s_ones + S::ONES;
-    uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_a + NW * NC * S::ABUF);
+    uint8_t* s_stage = s_a + NW * NC * S::ABUF;
+    uint32_t* s_pe = reinterpret_cast<uint32_t*>(s_stage + NW * NC * S::STAGE);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_pe + 32);
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + NC * NW);
 
@@ -285,6 +299,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     // uniform-register MMA issue (shuffled wg / TMEM base) and pipelined TMEM reads: mip
     // tiles and the compiled multi-material kernel; A/B-measured slower for the query kernel
     constexpr bool UNI = TILED || (MULTI && CT != 0);
+    constexpr bool TMA = TILED && S::TMA_OUT;  // mip tiles: staged output, one bulk store per tile
     const int wg = UNI ? __shfl_sync(0xffffffffu, warp >> 2, 0) : warp >> 2, q = warp & 3, row = q * 32 + lane;
 
     if (!MULTI)
@@ -347,6 +362,8 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         cx[c].id = c;
         cx[c].iq = (wg * NC + c) & 3;
         cx[c].adesc = umma_desc_k_sw128(cx[c].abuf);
+        cx[c].stage = smem_u32(s_stage + (wg * NC + c) * S::STAGE);
+        cx[c].ptile = -1;
         if (!MULTI) {
             cx[c].tile = (TILED || p.mode == 0 ? p.tile_first : 0) + ((int)blockIdx.x * NW + wg) * NC + c;
             if (cx[c].tile < ntiles) fetch_tile<P, MULTI, CT, TILED>(p, R, cx[c].tile, row, cx[c].nxt);
@@ -367,6 +384,10 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         tc_fence_before();
         handoff(C);
         if (q == C.iq && lane == 0) {
+            if (TMA && C.ptile >= 0) {  // the previous tile's staged output: one bulk store
+                bulk_s2g(p.out + (int64_t)C.ptile * TILE_M * (CT ? CT : p.c), C.stage, TILE_M * 2 * (CT ? CT : p.c));
+                bulk_commit();
+            }
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < 4; ++k) mma_f16_ss(C.tcol, C.adesc + (uint64_t)(k * 2), d_w1 + (uint64_t)(k * 2), ID64, k > 0);
@@ -377,6 +398,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
             }
             mma_commit(C.bar);
         }
+        C.ptile = -1;
         const int nt = C.tile + stride;
         if (nt < ntiles) fetch_tile<P, MULTI, CT, TILED>(p, R, nt, row, C.nxt);  // loads overlap the MLP
     };
@@ -396,6 +418,9 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         if (q == C.iq && lane == 0) {
             tc_fence_after();
             const bool last = layer == HM;
+            // the staging buffer is rewritten once this context's output MMA completes: its
+            // previous bulk store must have read it (issued two phases ago, normally done)
+            if (TMA && last) bulk_wait_read0();
             const uint64_t dl = last ? d_w3 : d_w2 + (uint64_t)((layer * S::W2_BYTES) >> 4);
             const uint32_t id = last ? ID16 : ID64;
 #pragma unroll
@@ -422,7 +447,14 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         for (int k = 0; k < (CT ? (CT + 1) / 2 : 8); ++k)
             o[k] = pack_half2(__saturatef(__uint_as_float(r[2 * k]) + (MULTI ? R.b3 : p.b3)[2 * k]),
                               __saturatef(__uint_as_float(r[2 * k + 1]) + (MULTI ? R.b3 : p.b3)[2 * k + 1]));
-        store_output<CT, TILED>(p, C.dst, C.flags & 1, C.flags & 2, !MULTI && C.tile < p.pair_tiles, row, o);  // R13: clamp [0,1]
+        if (TMA && C.tile < p.tma_tiles) {  // whole tile: rows into SMEM, stored by the next phase0
+            uint16_t* sdst = reinterpret_cast<uint16_t*>(s_stage + (size_t)(wg * NC + C.id) * S::STAGE) +
+                             row * (CT ? CT : p.c);
+            store_output<CT, TILED>(p, sdst, true, false, (CT ? CT : p.c) & 1, row, o);  // R13: clamp [0,1]
+            C.ptile = C.tile;
+        } else {
+            store_output<CT, TILED>(p, C.dst, C.flags & 1, C.flags & 2, !MULTI && C.tile < p.pair_tiles, row, o);
+        }
         tc_fence_before();
         C.tile += stride;
         phase0(C);
@@ -458,6 +490,20 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     };
     if constexpr (!MULTI) {
         run(0);  // tiles and their first fetches were set up with the contexts
+        if constexpr (TMA) {  // each context's last staged tile (its phase0 found no next tile)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                if (cx[c].ptile < 0) continue;
+                fence_proxy_async_smem();
+                handoff(cx[c]);
+                if (q == cx[c].iq && lane == 0) {
+                    bulk_s2g(p.out + (int64_t)cx[c].ptile * TILE_M * (CT ? CT : p.c), cx[c].stage,
+                             TILE_M * 2 * (CT ? CT : p.c));
+                    bulk_commit();
+                }
+            }
+            if (lane == 0) bulk_wait0();  // every bulk store complete before the CTA exits
+        }
     } else {
         // a contiguous share of the material-sorted tile list; one weight image at a time
         const int T = __ldg(mt->tstart + mt->n_mats);
