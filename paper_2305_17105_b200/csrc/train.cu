@@ -29,6 +29,12 @@ namespace ntc {
 
 constexpr int MAX_BOXES = 256;
 
+// phase of slot 0's first tile after which slot 1 starts (3: after the H1 epilogue, 5: after
+// the H2 epilogue, 7: after the loss; 0: both slots start together) -- see train_kernel
+#ifndef TRAIN_DESYNC
+#define TRAIN_DESYNC 5
+#endif
+
 struct Box {        // inclusive cell ranges of one grid
     int64_t off;    // element offset of the grid in the canonical latent array
     int32_t r, C, bits;
@@ -609,13 +615,13 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     int tile = blockIdx.x * SLOTS + slot;
     const int tstride = gridDim.x * SLOTS;
     Fetch F;
-#ifdef NTC_SLOT1_DELAY  // desynchronisation experiment (tools/trace_train.py only)
-    if (slot == 1) {
-        const long long t0 = clock64();
-        while (clock64() - t0 < NTC_SLOT1_DELAY) {
-        }
-    }
-#endif
+    // Slot desynchronisation: both slots run the same phase sequence, so started together they
+    // would stay phase-locked -- both waiting for MMAs at the same time, then competing for
+    // issue slots in their epilogues.  Slot 1 starts its first tile only when slot 0 passes
+    // phase TRAIN_DESYNC of its first tile (a named barrier: slot 1 sleeps, no issue slots).
+    constexpr int DESYNC = SLOTS == 2 ? TRAIN_DESYNC : 0;
+    if (DESYNC && slot == 1) named_bar_sync(3, 512);
+    if (DESYNC && slot == 0 && tile >= p.n_tiles) named_bar_arrive(3, 512);  // no first tile
     if (tile < p.n_tiles) fetch(tile, F);
     if (issuer) mbar_wait(s_wbar, 0);  // the weight images have landed (async proxy -> MMA reads)
     int iter = 0;
@@ -735,6 +741,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         NTC_TRACE(19);
         sync_slot();
         NTC_TRACE(3);
+        if (DESYNC == 3 && slot == 0 && iter == 0) named_bar_arrive(3, 512);
         // Z2 = H1 W2^T + b2
         if (issuer) {
             tc_fence_after();
@@ -761,6 +768,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         NTC_TRACE(21);
         sync_slot();
         NTC_TRACE(5);
+        if (DESYNC == 5 && slot == 0 && iter == 0) named_bar_arrive(3, 512);
         // Y = H_last W3^T + b3
         if (issuer) {
             tc_fence_after();
@@ -792,6 +800,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         NTC_TRACE(23);
         sync_slot();
         NTC_TRACE(7);
+        if (DESYNC == 7 && slot == 0 && iter == 0) named_bar_arrive(3, 512);
         // ---- t5: dH_last = d3 W3
         if (issuer) {
             tc_fence_after();

@@ -40,7 +40,7 @@ def run():
 
     import paper_2305_17105_b200 as ntc
 
-    ntc.LIB_PATH = TLIB
+    ntc.LIB_PATH = sys.argv[sys.argv.index("--lib") + 1] if "--lib" in sys.argv else TLIB
     L = ntc.lib()
     from paper_2305_17105_b200.synth import (SEED_BASE, Profile, gen_crops, gen_latents, gen_reference_u8,
                                              gen_weights_f32, u8_to_f16_bits)
