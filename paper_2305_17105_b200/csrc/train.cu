@@ -285,6 +285,7 @@ __device__ __forceinline__ void train_wimg_item_t(int i, const float* __restrict
 
 // t2: noisy = latent + U(-Q/2, Q/2) (one draw per latent per step), grad = 0, over the footprint
 __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
+    pdl_launch_dependents();  // the training kernel's CTAs may start their prologue meanwhile
     if ((int)blockIdx.x >= p.prep_blocks) {
         const int i = ((int)blockIdx.x - p.prep_blocks) * blockDim.x + threadIdx.x;
         if (p.wimg) {
@@ -417,15 +418,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     const int c = CT ? CT : p.c;
 
     // ---- weight images (fp16, built once per step by the trailing blocks of prep_kernel; the
-    // same images serve the backward MMAs through MN-major descriptors): one bulk TMA copy,
-    // waited by the MMA-issuing threads only, after the first tile's loads are in flight
+    // same images serve the backward MMAs through MN-major descriptors): one bulk TMA copy
+    // after the prologue, waited by the MMA-issuing threads only, after the first tile's loads
     uint64_t* s_wbar = s_bar + 2 * SLOTS;
-    if (tid == 0) {
-        mbar_init(s_wbar, 1);
-        fence_mbar_init();
-        mbar_arrive_expect_tx(s_wbar, S::WEND);
-        bulk_g2s(smem_u32(smem), p.wimg, S::WEND, s_wbar);
-    }
     if (tid < 32) s_pe[tid] = (&p.pe_words[0][0])[tid];
     if (tid < 4) s_loss[tid] = 0.0f;
     if (tid < NTC_MAX_CROPS) {
@@ -446,6 +441,16 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // launched programmatically after prep_kernel: the prologue above overlaps prep's tail;
+    // its outputs (weight image, noisy latents, zeroed latent gradients) are read only after
+    // this wait
+    pdl_wait();
+    if (tid == 0) {
+        mbar_init(s_wbar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(s_wbar, S::WEND);
+        bulk_g2s(smem_u32(smem), p.wimg, S::WEND, s_wbar);
+    }
     NTC_TRACE_K(1, (uint32_t)clock64());
 
     // TMEM per slot: depth 1: [0,128) dW-a accumulator, [128,144) dW-b, [192,256) scratch;
@@ -1024,6 +1029,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     }
 
     NTC_TRACE_K(2, (uint32_t)clock64());
+    pdl_launch_dependents();  // the reduce / Adam kernel may launch as CTAs retire
     if (pending_w) {
         mbar_wait(bar2, phase2);
         phase2 ^= 1;
@@ -1171,6 +1177,7 @@ __device__ __forceinline__ float reduce_block(const ReduceArgs& r, int blk, int&
 // (<= RED_MAXK) loads before summing them in order; the 8 group sums are then added in
 // order.  Block 0 also reduces the loss partials with a fixed-shape tree.
 __global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ ReduceArgs r) {
+    pdl_wait();  // the training kernel's partials are complete
     int i;
     reduce_block(r, blockIdx.x, i);
 }
@@ -1216,6 +1223,7 @@ __device__ __forceinline__ void adam_weight(const AdamParams& a, int64_t i, floa
 __device__ void adam_latent(const AdamParams& a, int64_t j);
 
 __global__ void adam_kernel(const __grid_constant__ AdamParams a) {
+    pdl_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < a.P) {  // weights: dense
         adam_weight(a, i, a.grad_par[i]);
@@ -1229,6 +1237,7 @@ __global__ void adam_kernel(const __grid_constant__ AdamParams a) {
 // blocks apply Adam to the footprint latents (their gradients are complete).
 __global__ void __launch_bounds__(256) reduce_adam_kernel(const __grid_constant__ ReduceArgs r,
                                                           const __grid_constant__ AdamParams a, int rblocks) {
+    pdl_wait();  // the training kernel's partials and latent gradients are complete
     if ((int)blockIdx.x < rblocks) {
         int i;
         const float g = reduce_block(r, blockIdx.x, i);
@@ -1304,6 +1313,24 @@ __device__ void adam_latent(const AdamParams& a, int64_t j) {
 
 // ====================================================================== host side
 using namespace ntc;
+
+// launch `kernel` so that it may start while the previous kernel of the stream finishes
+// (programmatic dependent launch; the kernel calls pdl_wait() before reading its inputs)
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, uint32_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 extern "C" int32_t ntc_num_mips(const ntc_desc* d);
 extern "C" int32_t ntc_num_levels(const ntc_desc* d);
@@ -1745,7 +1772,8 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
                                                 (tiles + slots - 1) / slots);
         e = ensure_smem((const void*)k, smem_bytes);
         if (e == cudaSuccess) {
-            k<<<grid, slots * 256, smem_bytes, st>>>(tp);
+            e = launch_pdl(k, grid, slots * 256, smem_bytes, st, tp);
+            if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
             // t6: deterministic cross-CTA reduction, scaled by 1/(B c); with APPLY in the same
             // call, t8 rides in the same launch (weights Adam'd as they are reduced)
             const ReduceArgs ra{t->partial,  (size_t)tp.Pst,  t->loss_partial, grid, (int)P, grid * slots,
@@ -1755,14 +1783,12 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
                 AdamParams a;
                 const int64_t nlat = build_adam(d, buf, boxes, hp, a);
                 if (nlat < 0) return FOOTPRINT_TOO_BIG();
-                reduce_adam_kernel<<<rblocks + (int)((nlat + 256 * LPT - 1) / (256 * LPT)), 256, 0, st>>>(ra, a,
-                                                                                                    rblocks);
-                e = cudaGetLastError();
+                e = launch_pdl(reduce_adam_kernel, rblocks + (int)((nlat + 256 * LPT - 1) / (256 * LPT)), 256, 0, st,
+                               ra, a, rblocks);
                 if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
                 return NTC_OK;
             }
-            reduce_kernel<<<rblocks, 256, 0, st>>>(ra);
-            e = cudaGetLastError();
+            e = launch_pdl(reduce_kernel, rblocks, 256, 0, st, ra);
         }
         if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
     }
