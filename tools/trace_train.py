@@ -89,7 +89,7 @@ def report(a):
     spans = []
     for b in range(nsm):
         for s in range(slots):
-            for it in range(iters - 1):
+            for it in range(iters - 2):
                 row = a[b, s, it]
                 if row[0, 0] == 0:
                     continue
@@ -108,6 +108,15 @@ def report(a):
     fin = ((k[..., 3] - k[..., 2]) % (1 << 32)).max(axis=(1, 2))
     print(f"per CTA cycles: prologue {pro.mean():.0f} (max {pro.max():.0f}), loop {loop.mean():.0f} "
           f"(min {loop.min():.0f} max {loop.max():.0f}), final {fin.mean():.0f} (max {fin.max():.0f})")
+    f = a[:, 0, 14, 0, :8]  # fused-step stamps (thread 0 per CTA), if any
+    if f[:, 0].any():
+        t0 = f[:, 0].min()
+        rel = (f - t0) % (1 << 32)
+        names = ["entry", "prep done", "grid sync 1", "train_body done", "grid sync 2", "weights reduce+Adam",
+                 "latent Adam"]
+        print("fused step, ns from the first CTA entry (mean / max over CTAs):")
+        for i, nm in enumerate(names):
+            print(f"  {nm:20s} {rel[:, i].mean():9.0f} {rel[:, i].max():9.0f}")
     g0 = k[..., 4].reshape(nsm, -1)
     g1 = k[..., 5].reshape(nsm, -1)
     t0 = g0.min()
