@@ -289,3 +289,42 @@ def test_fused_grads_apply_equals_split_calls(O):
         assert np.array_equal(out[0][k], out[1][k]), k
     for k in ("latents", "m_lat", "v_lat"):
         assert np.allclose(out[0][k], out[1][k], rtol=1e-4, atol=1e-9), k
+
+
+def test_train_step_cuda_graph_capture(O):
+    """A training step is CUDA-graph capturable: no host synchronisation or allocation on the
+    hot path (the bench / DP step can be replayed as a graph).  A graph of two steps (GRADS|APPLY,
+    then the split GRADS + APPLY calls of the data-parallel mode) replayed twice equals the same
+    four calls made directly, to fp32 rounding: the latent-gradient scatter's float atomics
+    make the latents run-order dependent in their last bits, and through the fp16 rounding of
+    the next step's inputs the weight updates too."""
+    d, lat, par, ref, crops = _setup(O, 128, 9, 78, 0, 3, 40)
+    refd = torch.from_numpy(ref.view(np.int16)).to(DEV)
+    batch = ntc.make_batch(0, gen_crops(400, 128, 0, 3, 40), refd, 128 * 9)
+    hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, 3, 5, 1, 0)
+    out = []
+    for graph in (False, True):
+        tr = ntc.Trainer(d)
+        t = _gpu_buffers(O, d, lat, par)
+        bufs = ntc.make_buffers(t)
+        loss = torch.zeros(1, device=DEV)
+
+        def two_steps():
+            ntc.ntc_train_step(tr, bufs, batch, hp, loss)
+            ntc.ntc_train_step(tr, bufs, batch, hp, loss, flags=ntc.NTC_STEP_GRADS)
+            ntc.ntc_train_step(tr, bufs, batch, hp, loss, flags=ntc.NTC_STEP_APPLY)
+
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                two_steps()
+            for _ in range(2):
+                g.replay()
+        else:
+            for _ in range(2):
+                two_steps()
+        torch.cuda.synchronize()
+        out.append({k: t[k].cpu().numpy().copy() for k in ("params", "m_par", "latents")})
+    for k in ("params", "m_par"):
+        assert np.allclose(out[0][k], out[1][k], rtol=1e-5, atol=1e-8), k
+    assert np.allclose(out[0]["latents"], out[1]["latents"], rtol=1e-4, atol=1e-9)

@@ -54,7 +54,7 @@ def summarise(rep):
 
 def main():
     out = sys.argv[1]
-    res = {"round": 1, "gpu": "NVIDIA B200 (sm_100a)",
+    res = {"round": 2, "gpu": "NVIDIA B200 (sm_100a)",
            "how": "ncu --set full --clock-control none --import-source on -k regex:<kernel> -s <skip> -c 1 "
                   "python bench.py --steps 1 --warmup 3 --no-cpu-baseline (one launch, replayed)",
            "kernels": {}}

@@ -2,7 +2,7 @@
 # Runs ON the GPU box (via gpurun): full GPU test suite, the default bench line, the ncu launch
 # list of a short bench run, and one `ncu --set full` capture per hot kernel.  Outputs land in
 # gpurun_out/ (scratch); tools/ncu_summary.py turns the captures into profiles/ncu_summary.json.
-TAG=${1:-r01}
+TAG=${1:-r02}
 O=gpurun_out
 timeout -s KILL 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu_$TAG.txt 2>&1
 tail -3 $O/pytest_gpu_$TAG.txt
