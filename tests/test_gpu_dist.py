@@ -299,3 +299,73 @@ def test_stacked_materials_match_single_process(world, mip, crop):
             assert np.allclose(p[k], t["params"].cpu().numpy(), rtol=1e-4, atol=1e-6)
             # latent bound: see test_sharded_dp_matches_single_process
             assert np.abs(full[k] - t["latents"].cpu().numpy()).max() <= 2e-3 * 0.01 * steps
+
+
+def _nccl_worker(q, steps, mip, crop):
+    """One rank over NCCL (a real NCCL communicator on cuda:0; two ranks cannot share one GPU
+    under NCCL): the device-side collectives of the sharded and stacked trainers run."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import paper_2305_17105_b200 as ntc
+        from paper_2305_17105_b200.dist import ShardedDataParallelTrainer, StackedDataParallelTrainer
+        from paper_2305_17105_b200.synth import gen_crops
+
+        assert dist.get_backend() == "nccl"
+        d, lat, par, ref = _setup_chain()
+        refd = torch.from_numpy(ref[mip].view(np.int16)).to(DEV)
+        sh = ShardedDataParallelTrainer(d, torch.from_numpy(lat.copy()).to(DEV), torch.from_numpy(par.copy()).to(DEV))
+        st = StackedDataParallelTrainer(d, [torch.from_numpy(lat.copy()).to(DEV)], [torch.from_numpy(par.copy()).to(DEV)])
+        out = []
+        for s in range(steps):
+            hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, s + 1, 7, 1, 0)
+            crops = gen_crops(40 + s, 128, mip, 6, crop)
+            l1 = float(sh.step(mip, crops, refd, (128 >> mip) * 8, hp).item())
+            l2 = float(st.step(mip, [crops], [refd], (128 >> mip) * 8, hp)[0].item())
+            out.append((l1, l2))
+        g = sh.gather_latents()  # the NCCL all-to-all of the band exchange
+        torch.cuda.synchronize()
+        q.put((out, sh.t["params"].cpu().numpy(), st.mats[0].t["params"].cpu().numpy(), g.cpu().numpy(),
+               sh.t["latents"].cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_single_rank_trainers():
+    """The NCCL code paths of dist.py (device all-reduce, all-to-all) on a one-rank NCCL group:
+    the sharded and the stacked trainer agree with each other and with single-process training
+    of the same batches (a one-rank all-reduce is the identity)."""
+    from paper_2305_17105_b200.synth import gen_crops
+
+    steps, mip, crop = 2, 1, 24
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(q, steps, mip, crop))
+    p.start()
+    out, p_sh, p_st, gathered, lat_sh = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    d, lat, par, ref = _setup_chain()
+    NL, P = lat.size, par.size
+    t = {k: torch.zeros(NL, device=DEV) for k in ("m_lat", "v_lat", "grad_lat", "noisy")}
+    t.update({k: torch.zeros(P, device=DEV) for k in ("m_par", "v_par", "grad_par")})
+    t["latents"] = torch.from_numpy(lat.copy()).to(DEV)
+    t["params"] = torch.from_numpy(par.copy()).to(DEV)
+    refd = torch.from_numpy(ref[mip].view(np.int16)).to(DEV)
+    tr, bufs, loss = ntc.Trainer(d), ntc.make_buffers(t), torch.zeros(1, device=DEV)
+    for s in range(steps):
+        hp = ntc.Hparams(0.01, 0.005, 0.9, 0.999, 1e-8, s + 1, 7, 1, 0)
+        ntc.ntc_train_step(tr, bufs, ntc.make_batch(mip, gen_crops(40 + s, 128, mip, 6, crop), refd, (128 >> mip) * 8),
+                           hp, loss)
+        assert abs(out[s][0] - float(loss.item())) <= 1e-5 * abs(float(loss.item()))
+        assert abs(out[s][1] - float(loss.item())) <= 1e-5 * abs(float(loss.item()))
+    torch.cuda.synchronize()
+    assert np.allclose(p_sh, t["params"].cpu().numpy(), rtol=1e-4, atol=1e-6)
+    assert np.allclose(p_st, p_sh, rtol=1e-4, atol=1e-6)
+    assert np.array_equal(gathered, lat_sh)  # one rank: the gathered bands are its own latents
+    assert np.abs(lat_sh - t["latents"].cpu().numpy()).max() <= 2e-3 * 0.01 * steps
