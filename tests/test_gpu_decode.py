@@ -336,3 +336,25 @@ def test_decode_texels_c16_alignment(O, off):
     assert np.all(got[:off] == -1.0) and np.all(got[off + n * 16:] == -1.0)
     ref = O.decode_texels(d, codes, w, allq)
     assert np.abs(got[off:off + n * 16].reshape(n, 16) - ref).max() <= TOL
+
+
+def test_maximum_texture_size(O):
+    """The largest texture the ABI accepts, 32768^2 (16 mips; NTC 0.2 level 0 alone holds
+    8192^2 x 8 G0 codes): random queries over every mip including the far corners (x, y =
+    32767 in the 16-bit query fields) and a whole mid mip, against the oracle."""
+    d = Profile.named("ntc0.2", 32768, 2)
+    mat, codes, w = _material(O, d, 0x4E5432)
+    q = gen_queries(91, 32768, 6000, "mip")
+    M = 16
+    corners = np.array([[(32768 >> m) - 1, (32768 >> m) - 1, m] for m in range(M)] +
+                       [[0, (32768 >> m) - 1, m] for m in range(M)], np.int32)
+    q = np.concatenate([q, corners])
+    got, st = _decode_queries_gpu(mat, q)
+    assert st == 0
+    ref = O.decode_texels(d, codes, w, q)
+    assert np.abs(got - ref).max() <= TOL
+    out = torch.empty((256 * 256 * 2,), dtype=torch.float16, device=DEV)
+    ntc.ntc_decode_mip(mat, 7, out)  # 256^2
+    torch.cuda.synchronize()
+    err = np.abs(out.float().cpu().numpy().reshape(256, 256, 2) - O.decode_mip(d, codes, w, 7))
+    assert err.max() <= TOL
