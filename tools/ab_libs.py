@@ -60,10 +60,30 @@ print(json.dumps({"train_us": _device_time(torch, run, flush, 50) * 1e6}))
 '''
 
 
+CHILD_RANDOM = r'''
+import sys, json, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2305_17105_b200 as ntc
+ntc.LIB_PATH = %r
+from bench import _device_time
+from paper_2305_17105_b200.synth import SEED_BASE, Profile, gen_codes, gen_queries, gen_weights_f16
+dev = torch.device("cuda", 0)
+d = Profile.named("ntc0.2", 4096, 16)
+mat = ntc.Material(d, torch.from_numpy(gen_codes(SEED_BASE + 2, ntc.grid_list(d))).to(dev),
+                   torch.from_numpy(gen_weights_f16(SEED_BASE + 3, d.input_dim, 16).view(np.int16)).to(dev))
+n = 1 << 24
+q = ntc.pack_queries(torch.from_numpy(gen_queries(SEED_BASE + 4, 4096, n, "area")).to(dev))
+out = torch.empty((n, 16), dtype=torch.float16, device=dev)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+t = _device_time(torch, lambda: ntc.ntc_decode_texels(mat, q, out), flush, 20)
+print(json.dumps({"random_c16": n / t / 1e9}))
+'''
+
+
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     rounds = int(sys.argv[sys.argv.index("--rounds") + 1]) if "--rounds" in sys.argv else 3
-    child = CHILD_TRAIN if "--train" in sys.argv else CHILD
+    child = CHILD_TRAIN if "--train" in sys.argv else (CHILD_RANDOM if "--random" in sys.argv else CHILD)
     libs = [a for a in args if a.endswith(".so")]
     res = {l: [] for l in libs}
     for _ in range(rounds):
