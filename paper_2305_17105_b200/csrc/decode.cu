@@ -118,6 +118,23 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, i
 #ifndef DECODE_TMA_OUT
 #define DECODE_TMA_OUT 0
 #endif
+// Where a context issues the latent loads of its next tile: 0 right after its MMA1 issue (end
+// of phase 0); 1 at the start of its second hidden phase, before that phase's MMA wait -- the
+// wait that otherwise has only the other context's first epilogue to hide behind (A/B: 1 is
+// 3-5% slower, the loads then land too late for the next assembly; 0 kept).
+// 1: the MMAs of the uniform-register instantiations are issued by the whole issuing warp
+// through elect.sync (no per-MMA single-thread waterfall); 0: by lane 0 of that warp
+#ifndef DECODE_WARP_ISSUE
+#define DECODE_WARP_ISSUE 1
+#endif
+// 1: a steady-state loop without the per-phase idle checks while every context holds a tile
+// (A/B: neutral on the chain decode, -4% on random queries; off)
+#ifndef DECODE_STEADY
+#define DECODE_STEADY 0
+#endif
+#ifndef DECODE_FETCH_AT
+#define DECODE_FETCH_AT 0
+#endif
 template <class P, int HM>
 struct DecodeSmem {
     // K1 > 64 (NTC 0.5 / 1.0 / 2.25): the K columns past 64 live in a K-major SW32 (K1 = 80)
@@ -343,6 +360,20 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
             named_bar_arrive(1 + wg * NC + C.id, 128);
     };
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
+    // MMA issue: whole warp (elect.sync) when the operands are provably warp-uniform
+    constexpr bool WI = DECODE_WARP_ISSUE && UNI;
+    auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        if constexpr (WI)
+            mma_f16_ss_warp(d, a, b, id, acc);
+        else
+            mma_f16_ss(d, a, b, id, acc);
+    };
+    auto commit = [&](uint64_t* bar) {
+        if constexpr (WI)
+            mma_commit_warp(bar);
+        else
+            mma_commit(bar);
+    };
     // single material: tiles blockIdx-strided over [first, ntiles); multi: per-run ranges
     int ntiles = TILED || p.mode == 0 ? p.n_tiles : (int)((p.nq + TILE_M - 1) / TILE_M);
     int stride = (int)gridDim.x * NW * NC;  // tiles advance by NC contexts per warpgroup
@@ -383,28 +414,35 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         fence_proxy_async_smem();
         tc_fence_before();
         handoff(C);
-        if (q == C.iq && lane == 0) {
-            if (TMA && C.ptile >= 0) {  // the previous tile's staged output: one bulk store
+        if (q == C.iq && (WI || lane == 0)) {
+            if (TMA && C.ptile >= 0 && lane == 0) {  // the previous tile's staged output: one bulk store
                 bulk_s2g(p.out + (int64_t)C.ptile * TILE_M * (CT ? CT : p.c), C.stage, TILE_M * 2 * (CT ? CT : p.c));
                 bulk_commit();
             }
             tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < 4; ++k) mma_f16_ss(C.tcol, C.adesc + (uint64_t)(k * 2), d_w1 + (uint64_t)(k * 2), ID64, k > 0);
+            for (int k = 0; k < 4; ++k) mma(C.tcol, C.adesc + (uint64_t)(k * 2), d_w1 + (uint64_t)(k * 2), ID64, k > 0);
             if constexpr (S::K2 > 0) {  // K columns 64 .. K1 - 1 from the SW32 / SW64 parts
                 const uint64_t a2 = S::K2B == 64 ? umma_desc_k_sw64(C.abuf + 128 * 128) : umma_desc_k_sw32(C.abuf + 128 * 128);
 #pragma unroll
-                for (int k = 0; k < S::K2 / 16; ++k) mma_f16_ss(C.tcol, a2 + (uint64_t)(k * 2), d_w1b + (uint64_t)(k * 2), ID64, 1);
+                for (int k = 0; k < S::K2 / 16; ++k) mma(C.tcol, a2 + (uint64_t)(k * 2), d_w1b + (uint64_t)(k * 2), ID64, 1);
             }
-            mma_commit(C.bar);
+            commit(C.bar);
         }
         C.ptile = -1;
-        const int nt = C.tile + stride;
-        if (nt < ntiles) fetch_tile<P, MULTI, CT, TILED>(p, R, nt, row, C.nxt);  // loads overlap the MLP
+        if (DECODE_FETCH_AT == 0) {
+            const int nt = C.tile + stride;
+            if (nt < ntiles) fetch_tile<P, MULTI, CT, TILED>(p, R, nt, row, C.nxt);  // loads overlap the MLP
+        }
     };
     // P1..P(HM+1): wait for the previous MMA, epilogue to the A tile, next layer's MMA
-    auto phase_hidden = [&](Ctx<P>& C, int layer) {
-        if (C.tile >= ntiles) return;
+    // chk = false: the caller knows the context holds a tile (steady-state loop below)
+    auto phase_hidden = [&](Ctx<P>& C, int layer, bool chk) {
+        if (chk && C.tile >= ntiles) return;
+        if (DECODE_FETCH_AT == 1 && layer == 1) {
+            const int nt = C.tile + stride;
+            if (nt < ntiles) fetch_tile<P, MULTI, CT, TILED>(p, R, nt, row, C.nxt);  // fills the MMA wait
+        }
         mbar_wait(C.bar, C.phase);
         C.phase ^= 1;
         tc_fence_after();
@@ -415,25 +453,25 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
         fence_proxy_async_smem();
         tc_fence_before();
         handoff(C);
-        if (q == C.iq && lane == 0) {
+        if (q == C.iq && (WI || lane == 0)) {
             tc_fence_after();
             const bool last = layer == HM;
             // the staging buffer is rewritten once this context's output MMA completes: its
             // previous bulk store must have read it (issued two phases ago, normally done)
-            if (TMA && last) bulk_wait_read0();
+            if (TMA && last && lane == 0) bulk_wait_read0();
             const uint64_t dl = last ? d_w3 : d_w2 + (uint64_t)((layer * S::W2_BYTES) >> 4);
             const uint32_t id = last ? ID16 : ID64;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) mma_f16_ss(C.tcol, C.adesc + 2 * k, dl + 2 * k, id, k > 0);
+            for (int k = 0; k < 4; ++k) mma(C.tcol, C.adesc + 2 * k, dl + 2 * k, id, k > 0);
             // hidden-layer bias: one K=16 MMA of the ones tile against the layer's SW32 bias
             // atom; the output bias is added in the output epilogue (FADD.SAT, free with the clamp)
-            if (!last) mma_f16_ss(C.tcol, d_ones, umma_desc_k_sw32(w2 + layer * S::W2_BYTES + 64 * 128), id, 1);
-            mma_commit(C.bar);
+            if (!last) mma(C.tcol, d_ones, umma_desc_k_sw32(w2 + layer * S::W2_BYTES + 64 * 128), id, 1);
+            commit(C.bar);
         }
     };
     // P(HM+2): wait for the output MMA, clamp, store, then start the context's next tile
-    auto phase_out = [&](Ctx<P>& C) {
-        if (C.tile >= ntiles) return;
+    auto phase_out = [&](Ctx<P>& C, bool chk) {
+        if (chk && C.tile >= ntiles) return;
         mbar_wait(C.bar, C.phase);
         C.phase ^= 1;
         tc_fence_after();
@@ -478,14 +516,26 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
             for (int c = 0; c < NC; ++c) b = b || cx[c].tile < ntiles;
             return b;
         };
+        // steady state: every context holds a tile (the last context's is the largest), so the
+        // phases skip their idle checks; the tail rounds check per context
+        if (DECODE_STEADY)
+            while (cx[NC - 1].tile < ntiles) {
+#pragma unroll
+                for (int layer = 0; layer <= HM; ++layer) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) phase_hidden(cx[c], layer, false);
+                }
+#pragma unroll
+                for (int c = 0; c < NC; ++c) phase_out(cx[c], false);
+            }
         while (busy()) {
 #pragma unroll
             for (int layer = 0; layer <= HM; ++layer) {
 #pragma unroll
-                for (int c = 0; c < NC; ++c) phase_hidden(cx[c], layer);
+                for (int c = 0; c < NC; ++c) phase_hidden(cx[c], layer, true);
             }
 #pragma unroll
-            for (int c = 0; c < NC; ++c) phase_out(cx[c]);
+            for (int c = 0; c < NC; ++c) phase_out(cx[c], true);
         }
     };
     if constexpr (!MULTI) {

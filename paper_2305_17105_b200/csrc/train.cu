@@ -34,6 +34,21 @@ constexpr int MAX_BOXES = 256;
 #ifndef TRAIN_DESYNC
 #define TRAIN_DESYNC 5
 #endif
+// 1: the backward MMAs (dH = delta W, dX = delta1 W1) accumulate in fp16 -- the delta epilogue
+// multiplies fp16(dH) by hardGELU' anyway, so it reads packed half2 words (no conversions), and
+// the latent-gradient run sums of the scatter run on half2 words (half the shuffles and adds);
+// 0: fp32 accumulators converted in the epilogues
+// 1: the output layer's weight-gradient MMAs (dW3/db3, 8 small MMAs) are issued with dH_last
+// instead of with dX, so fewer MMAs queue behind dX at the end of the tile
+#ifndef TRAIN_DWB_EARLY
+#define TRAIN_DWB_EARLY 0
+#endif
+#ifndef TRAIN_WARP_ISSUE
+#define TRAIN_WARP_ISSUE 0
+#endif
+#ifndef TRAIN_BWD_F16
+#define TRAIN_BWD_F16 1
+#endif
 
 struct Box {        // inclusive cell ranges of one grid
     int64_t off;    // element offset of the grid in the canonical latent array
@@ -466,7 +481,21 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     const uint32_t tH3 = tiles + S::H3 * S::TILE, tG3 = tiles + S::G3 * S::TILE;  // depth 2 only
     const uint32_t tHL = HM == 1 ? tH2 : tH3, tGL = HM == 1 ? tG2 : tG3;        // last hidden layer
     const uint32_t tXB = tX + (uint32_t)(KA - 1) * S::TILE;  // X atom holding the constant column D
-    const bool issuer = (warp & 7) == slot * 2 && lane == 0;  // the two issuers on different sub-partitions
+    // the two issuing warps sit on different sub-partitions; lane 0 issues (TRAIN_WARP_ISSUE = 1:
+    // the whole warp through elect.sync, as in decode -- measured slower here, 65.5 vs 64.3 us)
+    const bool issuer = (warp & 7) == slot * 2 && (TRAIN_WARP_ISSUE || lane == 0);
+    auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        if constexpr (TRAIN_WARP_ISSUE)
+            mma_f16_ss_warp(d, a, b, id, acc);
+        else
+            mma_f16_ss(d, a, b, id, acc);
+    };
+    auto commit = [&](uint64_t* mb) {
+        if constexpr (TRAIN_WARP_ISSUE)
+            mma_commit_warp(mb);
+        else
+            mma_commit(mb);
+    };
     uint64_t* bar = &s_bar[slot];
     uint64_t* bar2 = &s_bar[SLOTS + slot];
     uint32_t phase = 0, phase2 = 0;
@@ -499,7 +528,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     const uint64_t mG3 = umma_desc_mn_sw128(tG3, S::TILE);
     const uint64_t mD3 = umma_desc_mn_sw128(tD3, S::TILE);
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
-    constexpr uint32_t ID64_BT = idesc_f16(128, 64, false, true), IDX_BT = idesc_f16(128, NLATP, false, true);
+    constexpr bool BF16ACC = TRAIN_BWD_F16 != 0;  // fp16 accumulators of the backward MMAs
+    constexpr uint32_t ID64_BT = idesc_f16(128, 64, false, true, !BF16ACC);
+    constexpr uint32_t IDX_BT = idesc_f16(128, NLATP, false, true, !BF16ACC);
     constexpr uint32_t ID64_AB = idesc_f16(128, 64, true, true), ID16_AB = idesc_f16(128, 16, true, true);
     constexpr uint32_t ID128_AB = idesc_f16(128, 128, true, true);
 
@@ -703,9 +734,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < K1 / 16; ++kk)
-                mma_f16_ss(t_s, dX + (uint64_t)(((kk >> 2) * S::TILE + (kk & 3) * 32) >> 4),
+                mma(t_s, dX + (uint64_t)(((kk >> 2) * S::TILE + (kk & 3) * 32) >> 4),
                            dW1 + (uint64_t)(((kk >> 2) * 8192 + (kk & 3) * 32) >> 4), ID64, kk > 0);
-            mma_commit(bar);
+            commit(bar);
         }
         if (tile + tstride < p.n_tiles) fetch(tile + tstride, F);  // next tile's loads in flight
         wait_mma();
@@ -751,9 +782,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         if (issuer) {
             tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH1 + 2 * kk, dW2 + 2 * kk, ID64, kk > 0);
-            mma_f16_ss(t_s, dONES, dB2, ID64, 1);
-            mma_commit(bar);
+            for (int kk = 0; kk < 4; ++kk) mma(t_s, dH1 + 2 * kk, dW2 + 2 * kk, ID64, kk > 0);
+            mma(t_s, dONES, dB2, ID64, 1);
+            commit(bar);
         }
         wait_mma();
         NTC_TRACE(4);
@@ -763,9 +794,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             if (issuer) {
                 tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dH2 + 2 * kk, dW2B + 2 * kk, ID64, kk > 0);
-                mma_f16_ss(t_s, dONES, dB2B, ID64, 1);
-                mma_commit(bar);
+                for (int kk = 0; kk < 4; ++kk) mma(t_s, dH2 + 2 * kk, dW2B + 2 * kk, ID64, kk > 0);
+                mma(t_s, dONES, dB2B, ID64, 1);
+                commit(bar);
             }
             wait_mma();
             hidden_epilogue(tH3, tG3);
@@ -778,9 +809,9 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         if (issuer) {
             tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) mma_f16_ss(t_s, dHL + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
-            mma_f16_ss(t_s, dONES, dB3, ID16, 1);
-            mma_commit(bar);
+            for (int kk = 0; kk < 4; ++kk) mma(t_s, dHL + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
+            mma(t_s, dONES, dB3, ID16, 1);
+            commit(bar);
         }
         wait_mma();
         NTC_TRACE(6);
@@ -809,12 +840,43 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // ---- t5: dH_last = d3 W3
         if (issuer) {
             tc_fence_after();
-            mma_f16_ss(t_s, dD3, mW3, ID64_BT, 0);
-            mma_commit(bar);
+            mma(t_s, dD3, mW3, ID64_BT, 0);
+            commit(bar);
+            if (TRAIN_DWB_EARLY) {  // dW3/db3 += [X^T; H_last^T] delta3: its operands are final here
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma(t_acc_b, mXHL + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
+                               (!first || kk > 0) ? 1u : 0u);
+            }
         }
         wait_mma();
         NTC_TRACE(8);
         auto delta_epilogue = [&](uint32_t tG) {  // delta = fp16(dH) * hardGELU'(Z), in place
+            if constexpr (BF16ACC) {  // dH already fp16: two packed 16-column loads per half
+                uint32_t r[2][8];
+                tmem_ld8_pack(t_s + lane_off + 32 * h, r[0]);
+                tmem_wait_ld_r8(r[0]);
+                tmem_ld8_pack(t_s + lane_off + 32 * h + 16, r[1]);
+#pragma unroll
+                for (int part = 0; part < 2; ++part) {
+                    if (part == 1) tmem_wait_ld_r8(r[1]);
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) {
+                        const int ch = 4 * h + 2 * part + cc;
+                        const uint4 gq = lds_row_chunk(tG, row, ch);
+                        const uint32_t gw[4] = {gq.x, gq.y, gq.z, gq.w};
+                        uint32_t o[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const __half2 dv = __hmul2(*reinterpret_cast<const __half2*>(&r[part][4 * cc + e]),
+                                                       *reinterpret_cast<const __half2*>(&gw[e]));
+                            o[e] = *reinterpret_cast<const uint32_t*>(&dv);
+                        }
+                        sts_row_chunk(tG, row, ch, o[0], o[1], o[2], o[3]);
+                    }
+                }
+                return;
+            }
             uint32_t r[2][16];
             tmem_ld16(t_s + lane_off + 32 * h, r[0]);
             tmem_wait_ld_r16(r[0]);
@@ -847,8 +909,8 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    mma_f16_ss(t_s, dG3 + 2 * kk, mW2B + (uint64_t)(kk * 128), ID64_BT, kk > 0);
-                mma_commit(bar);
+                    mma(t_s, dG3 + 2 * kk, mW2B + (uint64_t)(kk * 128), ID64_BT, kk > 0);
+                commit(bar);
             }
             wait_mma();
             delta_epilogue(tG2);
@@ -861,8 +923,8 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                mma_f16_ss(t_s, dG2 + 2 * kk, mW2 + (uint64_t)(kk * 128), ID64_BT, kk > 0);
-            mma_commit(bar);
+                mma(t_s, dG2 + 2 * kk, mW2 + (uint64_t)(kk * 128), ID64_BT, kk > 0);
+            commit(bar);
         }
         wait_mma();
         NTC_TRACE(10);
@@ -875,18 +937,20 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                mma_f16_ss(t_s, dG1 + 2 * kk, mW1 + (uint64_t)(kk * 128), IDX_BT, kk > 0);
-            mma_commit(bar);
+                mma(t_s, dG1 + 2 * kk, mW1 + (uint64_t)(kk * 128), IDX_BT, kk > 0);
+            commit(bar);
             // weight gradients, off the critical path: they run while this tile scatters and
             // the next tile fetches; bar2 is waited before the next tile overwrites the tiles
+            if (!TRAIN_DWB_EARLY) {
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-                mma_f16_ss(t_acc_b, mXHL + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
-                           (!first || kk > 0) ? 1u : 0u);
+                for (int kk = 0; kk < 8; ++kk)
+                    mma(t_acc_b, mXHL + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
+                               (!first || kk > 0) ? 1u : 0u);
+            }
             if constexpr (HM == 2) {  // dW2b/db2b += [X^T; H2^T] delta3h
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_f16_ss(t_acc_m, mXH2 + (uint64_t)(kk * 128), mG3 + (uint64_t)(kk * 128), ID64_AB,
+                    mma(t_acc_m, mXH2 + (uint64_t)(kk * 128), mG3 + (uint64_t)(kk * 128), ID64_AB,
                                (!first || kk > 0) ? 1u : 0u);
             }
             if constexpr (KA == 1) {
@@ -895,20 +959,20 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                 // and rows < 64 of the delta2 half except the constant row are not)
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_f16_ss(t_acc_a, mXH1 + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID128_AB,
+                    mma(t_acc_a, mXH1 + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID128_AB,
                                (!first || kk > 0) ? 1u : 0u);
             } else {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_f16_ss(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
+                    mma(t_acc_a + 64, mXH1 + (uint64_t)(kk * 128), mG2 + (uint64_t)(kk * 128), ID64_AB,
                                (!first || kk > 0) ? 1u : 0u);
                 // dW1/db1: [X0^T; X1^T] delta1
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_f16_ss(t_acc_a, mXX + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID64_AB,
+                    mma(t_acc_a, mXX + (uint64_t)(kk * 128), mG1 + (uint64_t)(kk * 128), ID64_AB,
                                (!first || kk > 0) ? 1u : 0u);
             }
-            mma_commit(bar2);
+            commit(bar2);
         }
         wait_mma();
         NTC_TRACE(12);
@@ -919,7 +983,135 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // four G0 cells and runs of 8 share the G1 cells at LOD 0), so each run is summed to its
         // first lane with two (G0) / three (G1) shuffle steps and only run heads issue the
         // vector reductions -- no global contention storm.
-        {
+        if constexpr (BF16ACC) {
+            // dX is fp16 in TMEM: the run sums run on packed half2 words (channel pairs), then
+            // widen to fp32 for the scaled vector reductions (the fp16 run sums of <= 4 / 8 texels
+            // add one rounding, far inside the gradient tolerance R21)
+            const float s = p.inv_bc;
+            const bool on = valid && !p.freeze;
+            if (h == 0) {
+                constexpr int NW0 = 2 * C0;  // words of the 4 x C0 G0 values (tap-major)
+                uint32_t g0w[NW0];
+#pragma unroll
+                for (int w = 0; w + 16 <= NW0; w += 16) {
+                    uint32_t q[16];
+                    tmem_ld16_pack(t_s + lane_off + 2 * w, q);
+                    tmem_wait_ld_r16(q);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) g0w[w + e] = on ? q[e] : 0u;
+                }
+                if constexpr (NW0 % 16 == 8) {
+                    uint32_t q[8];
+                    tmem_ld8_pack(t_s + lane_off + 2 * (NW0 - 8), q);
+                    tmem_wait_ld_r8(q);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) g0w[NW0 - 8 + e] = on ? q[e] : 0u;
+                }
+                int tx0[2], ty0[2];
+                taps_g0(T, tx0, ty0);
+                float* gl0 = p.grad_lat + p.off0;
+                const uint32_t kx0 = on ? (uint32_t)(tx0[0] | (tx0[1] << 16)) : 0xFFFFFFF0u - lane;
+                const uint32_t ky0 = (uint32_t)(ty0[0] | (ty0[1] << 16));
+#pragma unroll
+                for (int d = 1; d <= 2; d <<= 1) {
+                    const uint32_t nx0 = __shfl_down_sync(0xffffffffu, kx0, d);
+                    const uint32_t ny0 = __shfl_down_sync(0xffffffffu, ky0, d);
+                    const bool s0 = lane + d < 32 && nx0 == kx0 && ny0 == ky0;
+#pragma unroll
+                    for (int i = 0; i < NW0; ++i) {
+                        const uint32_t o = __shfl_down_sync(0xffffffffu, g0w[i], d);
+                        const __half2 sum = __hadd2(*reinterpret_cast<const __half2*>(&g0w[i]),
+                                                    *reinterpret_cast<const __half2*>(&o));
+                        if (s0) g0w[i] = *reinterpret_cast<const uint32_t*>(&sum);
+                    }
+                }
+                const uint32_t px0 = __shfl_up_sync(0xffffffffu, kx0, 1), py0 = __shfl_up_sync(0xffffffffu, ky0, 1);
+                if (on && (lane == 0 || px0 != kx0 || py0 != ky0)) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        float* dst = gl0 + ((int64_t)ty0[t >> 1] * p.r0 + tx0[t & 1]) * C0;
+#pragma unroll
+                        for (int e = 0; e < C0; e += 4) {
+                            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&g0w[(t * C0 + e) / 2]));
+                            const float2 b =
+                                __half22float2(*reinterpret_cast<const __half2*>(&g0w[(t * C0 + e) / 2 + 1]));
+                            red_add_v4(dst + e, s * a.x, s * a.y, s * b.x, s * b.y);
+                        }
+                    }
+                }
+            } else {
+                constexpr int NW1 = C1 / 2;
+                constexpr int NQ = NW1 <= 8 ? 8 : 16;
+                uint32_t q[NQ];
+                if constexpr (NQ == 8) {
+                    tmem_ld8_pack(t_s + lane_off + 4 * C0, *reinterpret_cast<uint32_t(*)[8]>(q));
+                    tmem_wait_ld_r8(*reinterpret_cast<uint32_t(*)[8]>(q));
+                } else {
+                    tmem_ld16_pack(t_s + lane_off + 4 * C0, *reinterpret_cast<uint32_t(*)[16]>(q));
+                    tmem_wait_ld_r16(*reinterpret_cast<uint32_t(*)[16]>(q));
+                }
+                int tx1[2], ty1[2];
+                uint32_t axq, ayq;
+                taps_g1(T, tx1, ty1, axq, ayq);
+                float* gl1 = p.grad_lat + p.off1;
+                const uint32_t kx1 = on ? (uint32_t)(tx1[0] | (tx1[1] << 16)) : 0xFFFFFFF0u - lane;
+                const uint32_t ky1 = (uint32_t)T.y;
+                const uint32_t ky1b = (uint32_t)(ty1[0] | (ty1[1] << 16));
+                // x-weights (multiples of 1/16, exact in fp16) applied per texel, y-weights at the head
+                const float ax = (float)axq * (1.0f / 16.0f);
+                const float ay = (float)ayq * (1.0f / 16.0f);
+                const __half2 wa = __float2half2_rn(1.0f - ax), wb = __float2half2_rn(ax);
+                uint32_t g1w[2 * NW1];
+#pragma unroll
+                for (int e = 0; e < NW1; ++e) {
+                    const __half2 v = *reinterpret_cast<const __half2*>(&q[e]);
+                    const __half2 va = __hmul2(v, wa), vb = __hmul2(v, wb);
+                    g1w[e] = on ? *reinterpret_cast<const uint32_t*>(&va) : 0u;
+                    g1w[NW1 + e] = on ? *reinterpret_cast<const uint32_t*>(&vb) : 0u;
+                }
+#pragma unroll
+                for (int d = 1; d <= 4; d <<= 1) {
+                    const uint32_t nx1 = __shfl_down_sync(0xffffffffu, kx1, d);
+                    const uint32_t ny1 = __shfl_down_sync(0xffffffffu, ky1, d);
+                    const uint32_t ny1b = __shfl_down_sync(0xffffffffu, ky1b, d);
+                    const bool s1 = lane + d < 32 && nx1 == kx1 && ny1 == ky1 && ny1b == ky1b;
+#pragma unroll
+                    for (int i = 0; i < 2 * NW1; ++i) {
+                        const uint32_t o = __shfl_down_sync(0xffffffffu, g1w[i], d);
+                        const __half2 sum = __hadd2(*reinterpret_cast<const __half2*>(&g1w[i]),
+                                                    *reinterpret_cast<const __half2*>(&o));
+                        if (s1) g1w[i] = *reinterpret_cast<const uint32_t*>(&sum);
+                    }
+                }
+                const uint32_t px1 = __shfl_up_sync(0xffffffffu, kx1, 1), py1 = __shfl_up_sync(0xffffffffu, ky1, 1);
+                const uint32_t py1b = __shfl_up_sync(0xffffffffu, ky1b, 1);
+                if (on && (lane == 0 || px1 != kx1 || py1 != ky1 || py1b != ky1b)) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float wy = (t >> 1) ? ay : 1.0f - ay;
+                        const uint32_t* Sv = g1w + (t & 1) * NW1;
+                        float* dst = gl1 + ((int64_t)ty1[t >> 1] * p.r1 + tx1[t & 1]) * C1;
+                        const float sw = s * wy;
+                        if (sw != 0.0f) {
+                            if constexpr (C1 % 4 == 0) {
+#pragma unroll
+                                for (int e = 0; e < C1; e += 4) {
+                                    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&Sv[e / 2]));
+                                    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&Sv[e / 2 + 1]));
+                                    red_add_v4(dst + e, sw * a.x, sw * a.y, sw * b.x, sw * b.y);
+                                }
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < C1; e += 2) {
+                                    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&Sv[e / 2]));
+                                    red_add_v2(dst + e, sw * a.x, sw * a.y);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        } else {
             const float s = p.inv_bc;
             const bool on = valid && !p.freeze;
             if (h == 0) {
