@@ -123,12 +123,17 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, i
 // wait that otherwise has only the other context's first epilogue to hide behind (A/B: 1 is
 // 3-5% slower, the loads then land too late for the next assembly; 0 kept).
 // 1: the MMAs of the uniform-register instantiations are issued by the whole issuing warp
-// through elect.sync (no per-MMA single-thread waterfall); 0: by lane 0 of that warp
+// through elect.sync (no per-MMA single-thread waterfall); 2: and each layer's MMAs + commit as
+// one asm block; 0: by lane 0 of that warp.  A/B on the 4K chain (3 rounds): 0 -> 1: c = 9
+// 29.85 -> 30.61 Gtexel/s; 1 -> 2: c = 9 30.44 -> 32.34, c = 16 30.08 -> 32.34
 #ifndef DECODE_WARP_ISSUE
-#define DECODE_WARP_ISSUE 1
+#define DECODE_WARP_ISSUE 2
 #endif
 // 1: a steady-state loop without the per-phase idle checks while every context holds a tile
 // (A/B: neutral on the chain decode, -4% on random queries; off)
+#ifndef DECODE_WARP_ALL
+#define DECODE_WARP_ALL 0
+#endif
 #ifndef DECODE_STEADY
 #define DECODE_STEADY 0
 #endif
@@ -361,7 +366,10 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     };
     constexpr uint32_t ID64 = idesc_f16(128, 64), ID16 = idesc_f16(128, 16);
     // MMA issue: whole warp (elect.sync) when the operands are provably warp-uniform
-    constexpr bool WI = DECODE_WARP_ISSUE && UNI;
+    // (DECODE_WARP_ALL: also the instantiations whose operands are not provably uniform; ptxas
+    // then broadcasts them from the elected lane -- A/B: random queries 20.5 -> 18.5, off)
+    constexpr bool WI = DECODE_WARP_ISSUE && (UNI || DECODE_WARP_ALL);
+    constexpr bool WG4 = WI && DECODE_WARP_ISSUE >= 2;  // whole layers as one asm block
     auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
         if constexpr (WI)
             mma_f16_ss_warp(d, a, b, id, acc);
@@ -420,14 +428,24 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
                 bulk_commit();
             }
             tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < 4; ++k) mma(C.tcol, C.adesc + (uint64_t)(k * 2), d_w1 + (uint64_t)(k * 2), ID64, k > 0);
-            if constexpr (S::K2 > 0) {  // K columns 64 .. K1 - 1 from the SW32 / SW64 parts
+            if constexpr (WG4 && S::K2 == 0) {  // the whole layer in one asm block
+                mma4_commit_warp<false>(C.tcol, C.adesc, d_w1, ID64, 0, 0, C.bar);
+            } else if constexpr (WG4) {  // K1 > 64: the SW128 atom's chain, then the SW32 / SW64 part
+                mma_chain4_warp<2, 2>(C.tcol, C.adesc, d_w1, ID64, 0);
                 const uint64_t a2 = S::K2B == 64 ? umma_desc_k_sw64(C.abuf + 128 * 128) : umma_desc_k_sw32(C.abuf + 128 * 128);
+                if constexpr (S::K2 == 32) mma_f16_ss_warp(C.tcol, a2, d_w1b, ID64, 1);
+                mma1_commit_warp(C.tcol, a2 + (S::K2 == 32 ? 2 : 0), d_w1b + (S::K2 == 32 ? 2 : 0), ID64, 1, C.bar);
+            } else {
 #pragma unroll
-                for (int k = 0; k < S::K2 / 16; ++k) mma(C.tcol, a2 + (uint64_t)(k * 2), d_w1b + (uint64_t)(k * 2), ID64, 1);
+                for (int k = 0; k < 4; ++k) mma(C.tcol, C.adesc + (uint64_t)(k * 2), d_w1 + (uint64_t)(k * 2), ID64, k > 0);
+                if constexpr (S::K2 > 0) {  // K columns 64 .. K1 - 1 from the SW32 / SW64 parts
+                    const uint64_t a2 =
+                        S::K2B == 64 ? umma_desc_k_sw64(C.abuf + 128 * 128) : umma_desc_k_sw32(C.abuf + 128 * 128);
+#pragma unroll
+                    for (int k = 0; k < S::K2 / 16; ++k) mma(C.tcol, a2 + (uint64_t)(k * 2), d_w1b + (uint64_t)(k * 2), ID64, 1);
+                }
+                commit(C.bar);
             }
-            commit(C.bar);
         }
         C.ptile = -1;
         if (DECODE_FETCH_AT == 0) {
@@ -461,12 +479,20 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
             if (TMA && last && lane == 0) bulk_wait_read0();
             const uint64_t dl = last ? d_w3 : d_w2 + (uint64_t)((layer * S::W2_BYTES) >> 4);
             const uint32_t id = last ? ID16 : ID64;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) mma(C.tcol, C.adesc + 2 * k, dl + 2 * k, id, k > 0);
             // hidden-layer bias: one K=16 MMA of the ones tile against the layer's SW32 bias
             // atom; the output bias is added in the output epilogue (FADD.SAT, free with the clamp)
-            if (!last) mma(C.tcol, d_ones, umma_desc_k_sw32(w2 + layer * S::W2_BYTES + 64 * 128), id, 1);
-            commit(C.bar);
+            if constexpr (WG4) {
+                if (last)
+                    mma4_commit_warp<false>(C.tcol, C.adesc, dl, id, 0, 0, C.bar);
+                else
+                    mma4_commit_warp<true>(C.tcol, C.adesc, dl, id, d_ones,
+                                           umma_desc_k_sw32(w2 + layer * S::W2_BYTES + 64 * 128), C.bar);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mma(C.tcol, C.adesc + 2 * k, dl + 2 * k, id, k > 0);
+                if (!last) mma(C.tcol, d_ones, umma_desc_k_sw32(w2 + layer * S::W2_BYTES + 64 * 128), id, 1);
+                commit(C.bar);
+            }
         }
     };
     // P(HM+2): wait for the output MMA, clamp, store, then start the context's next tile

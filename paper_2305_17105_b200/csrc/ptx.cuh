@@ -160,6 +160,158 @@ __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
         : "memory");
 }
 
+// One whole layer in one asm block (whole converged warp, lane 0 elected): four K = 16 steps
+// of D (+)= A B^T with both K-major descriptors advancing 32 bytes (2 units) per step, then
+// optionally one more MMA (the ones x bias atom of a hidden layer), then the commit to `bar`.
+// A single elect and one conversion of each base operand for the whole group.
+#define NTC_MMA4_HEAD                                                                              \
+    "{\n\t.reg .pred e, t, f;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"                            \
+    "elect.sync _|e, 0xffffffff;\n\t"                                                               \
+    "setp.eq.u32 t, 0, 0;\n\t"                                                                      \
+    "setp.ne.u32 f, 0, 0;\n\t"                                                                      \
+    "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"                            \
+    "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"                            \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n\t"                                 \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"                                 \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"                                 \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t"
+template <bool BIAS>
+__device__ __forceinline__ void mma4_commit_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint64_t ones,
+                                                 uint64_t bias, uint64_t* bar) {
+    if constexpr (BIAS)
+        asm volatile(NTC_MMA4_HEAD
+                     "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %5, %3, t;\n\t"
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}" ::"r"(d),
+                     "l"(a), "l"(b), "r"(idesc), "l"(ones), "l"(bias), "r"(smem_u32(bar))
+                     : "memory");
+    else
+        asm volatile(NTC_MMA4_HEAD
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}" ::"r"(d),
+                     "l"(a), "l"(b), "r"(idesc), "r"(smem_u32(bar))
+                     : "memory");
+}
+
+// A chain of N K-steps of D (+)= A B^T in one asm block (whole converged warp, lane 0 elected):
+// step i uses descriptors a + i*AST, b + i*BST (16-byte units); the first step accumulates when
+// acc0 != 0, the others always; optionally the commit to `bar`.  One elect and one conversion of
+// each base operand for the whole chain (the per-MMA form costs ~6 instructions per MMA).
+#define NTC_CHAIN4(AS1, BS1, AS2, BS2, AS3, BS3) \
+    "{\n\t.reg .pred e, t, p;\n\t.reg .b64 a1, b1, a2, b2, a3, b3;\n\t" \
+    "elect.sync _|e, 0xffffffff;\n\t" \
+    "setp.eq.u32 t, 0, 0;\n\t" \
+    "setp.ne.b32 p, %4, 0;\n\t" \
+    "add.s64 a1, %1, " #AS1 ";\n\tadd.s64 b1, %2, " #BS1 ";\n\t" \
+    "add.s64 a2, %1, " #AS2 ";\n\tadd.s64 b2, %2, " #BS2 ";\n\t" \
+    "add.s64 a3, %1, " #AS3 ";\n\tadd.s64 b3, %2, " #BS3 ";\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t" \
+    "}"
+
+#define NTC_CHAIN4_C(AS1, BS1, AS2, BS2, AS3, BS3) \
+    "{\n\t.reg .pred e, t, p;\n\t.reg .b64 a1, b1, a2, b2, a3, b3;\n\t" \
+    "elect.sync _|e, 0xffffffff;\n\t" \
+    "setp.eq.u32 t, 0, 0;\n\t" \
+    "setp.ne.b32 p, %4, 0;\n\t" \
+    "add.s64 a1, %1, " #AS1 ";\n\tadd.s64 b1, %2, " #BS1 ";\n\t" \
+    "add.s64 a2, %1, " #AS2 ";\n\tadd.s64 b2, %2, " #BS2 ";\n\t" \
+    "add.s64 a3, %1, " #AS3 ";\n\tadd.s64 b3, %2, " #BS3 ";\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t" \
+    "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t" \
+    "}"
+
+#define NTC_CHAIN8(AS1, BS1, AS2, BS2, AS3, BS3, AS4, BS4, AS5, BS5, AS6, BS6, AS7, BS7) \
+    "{\n\t.reg .pred e, t, p;\n\t.reg .b64 a1, b1, a2, b2, a3, b3, a4, b4, a5, b5, a6, b6, a7, b7;\n\t" \
+    "elect.sync _|e, 0xffffffff;\n\t" \
+    "setp.eq.u32 t, 0, 0;\n\t" \
+    "setp.ne.b32 p, %4, 0;\n\t" \
+    "add.s64 a1, %1, " #AS1 ";\n\tadd.s64 b1, %2, " #BS1 ";\n\t" \
+    "add.s64 a2, %1, " #AS2 ";\n\tadd.s64 b2, %2, " #BS2 ";\n\t" \
+    "add.s64 a3, %1, " #AS3 ";\n\tadd.s64 b3, %2, " #BS3 ";\n\t" \
+    "add.s64 a4, %1, " #AS4 ";\n\tadd.s64 b4, %2, " #BS4 ";\n\t" \
+    "add.s64 a5, %1, " #AS5 ";\n\tadd.s64 b5, %2, " #BS5 ";\n\t" \
+    "add.s64 a6, %1, " #AS6 ";\n\tadd.s64 b6, %2, " #BS6 ";\n\t" \
+    "add.s64 a7, %1, " #AS7 ";\n\tadd.s64 b7, %2, " #BS7 ";\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, t;\n\t" \
+    "}"
+
+#define NTC_CHAIN8_C(AS1, BS1, AS2, BS2, AS3, BS3, AS4, BS4, AS5, BS5, AS6, BS6, AS7, BS7) \
+    "{\n\t.reg .pred e, t, p;\n\t.reg .b64 a1, b1, a2, b2, a3, b3, a4, b4, a5, b5, a6, b6, a7, b7;\n\t" \
+    "elect.sync _|e, 0xffffffff;\n\t" \
+    "setp.eq.u32 t, 0, 0;\n\t" \
+    "setp.ne.b32 p, %4, 0;\n\t" \
+    "add.s64 a1, %1, " #AS1 ";\n\tadd.s64 b1, %2, " #BS1 ";\n\t" \
+    "add.s64 a2, %1, " #AS2 ";\n\tadd.s64 b2, %2, " #BS2 ";\n\t" \
+    "add.s64 a3, %1, " #AS3 ";\n\tadd.s64 b3, %2, " #BS3 ";\n\t" \
+    "add.s64 a4, %1, " #AS4 ";\n\tadd.s64 b4, %2, " #BS4 ";\n\t" \
+    "add.s64 a5, %1, " #AS5 ";\n\tadd.s64 b5, %2, " #BS5 ";\n\t" \
+    "add.s64 a6, %1, " #AS6 ";\n\tadd.s64 b6, %2, " #BS6 ";\n\t" \
+    "add.s64 a7, %1, " #AS7 ";\n\tadd.s64 b7, %2, " #BS7 ";\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, t;\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, t;\n\t" \
+    "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t" \
+    "}"
+
+// chains of 4 / 8 K-steps (steps in 16-byte descriptor units), with or without the commit
+template <int AS, int BS>
+__device__ __forceinline__ void mma_chain4_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(NTC_CHAIN4(%5, %6, %7, %8, %9, %10)::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc0), "n"(AS), "n"(BS),
+                 "n"(2 * AS), "n"(2 * BS), "n"(3 * AS), "n"(3 * BS)
+                 : "memory");
+}
+template <int AS, int BS>
+__device__ __forceinline__ void mma_chain4_commit_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                       uint32_t acc0, uint64_t* bar) {
+    asm volatile(NTC_CHAIN4_C(%6, %7, %8, %9, %10, %11)::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc0),
+                 "r"(smem_u32(bar)), "n"(AS), "n"(BS), "n"(2 * AS), "n"(2 * BS), "n"(3 * AS), "n"(3 * BS)
+                 : "memory");
+}
+template <int AS, int BS>
+__device__ __forceinline__ void mma_chain8_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(NTC_CHAIN8(%5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18)::"r"(d), "l"(a), "l"(b),
+                 "r"(idesc), "r"(acc0), "n"(AS), "n"(BS), "n"(2 * AS), "n"(2 * BS), "n"(3 * AS), "n"(3 * BS),
+                 "n"(4 * AS), "n"(4 * BS), "n"(5 * AS), "n"(5 * BS), "n"(6 * AS), "n"(6 * BS), "n"(7 * AS), "n"(7 * BS)
+                 : "memory");
+}
+template <int AS, int BS>
+__device__ __forceinline__ void mma_chain8_commit_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                       uint32_t acc0, uint64_t* bar) {
+    asm volatile(NTC_CHAIN8_C(%6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19)::"r"(d), "l"(a),
+                 "l"(b), "r"(idesc), "r"(acc0), "r"(smem_u32(bar)), "n"(AS), "n"(BS), "n"(2 * AS), "n"(2 * BS),
+                 "n"(3 * AS), "n"(3 * BS), "n"(4 * AS), "n"(4 * BS), "n"(5 * AS), "n"(5 * BS), "n"(6 * AS), "n"(6 * BS),
+                 "n"(7 * AS), "n"(7 * BS)
+                 : "memory");
+}
+// one MMA (enable-input-d = acc) and the commit to `bar`, whole warp
+__device__ __forceinline__ void mma1_commit_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                                 uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -43,8 +43,8 @@ constexpr int MAX_BOXES = 256;
 #ifndef TRAIN_DWB_EARLY
 #define TRAIN_DWB_EARLY 0
 #endif
-#ifndef TRAIN_WARP_ISSUE
-#define TRAIN_WARP_ISSUE 0
+#ifndef TRAIN_WARP_ISSUE  // see train_kernel
+#define TRAIN_WARP_ISSUE 2
 #endif
 #ifndef TRAIN_BWD_F16
 #define TRAIN_BWD_F16 1
@@ -481,9 +481,13 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     const uint32_t tH3 = tiles + S::H3 * S::TILE, tG3 = tiles + S::G3 * S::TILE;  // depth 2 only
     const uint32_t tHL = HM == 1 ? tH2 : tH3, tGL = HM == 1 ? tG2 : tG3;        // last hidden layer
     const uint32_t tXB = tX + (uint32_t)(KA - 1) * S::TILE;  // X atom holding the constant column D
-    // the two issuing warps sit on different sub-partitions; lane 0 issues (TRAIN_WARP_ISSUE = 1:
-    // the whole warp through elect.sync, as in decode -- measured slower here, 65.5 vs 64.3 us)
+    // the two issuing warps sit on different sub-partitions.  TRAIN_WARP_ISSUE 0: lane 0 issues
+    // each MMA (a single-thread waterfall around every tcgen05.mma); 1: the whole warp through
+    // elect.sync, per MMA (measured slower: 65.5 vs 64.3 us); 2 (default): the whole warp, each
+    // MMA group one asm block (one elect per group): 63.2 vs 64.4 us per C4 step (A/B, 3 rounds)
     const bool issuer = (warp & 7) == slot * 2 && (TRAIN_WARP_ISSUE || lane == 0);
+    // TRAIN_WARP_ISSUE = 2: each MMA group of the depth-1, K1 = 64 kernel as one asm block
+    constexpr bool CH = TRAIN_WARP_ISSUE >= 2 && HM == 1 && KA == 1;
     auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
         if constexpr (TRAIN_WARP_ISSUE)
             mma_f16_ss_warp(d, a, b, id, acc);
@@ -732,11 +736,15 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // ---- t3: forward.  Z1 = X W1^T (+b1)
         if (issuer) {
             tc_fence_after();
+            if constexpr (CH) {
+                mma_chain4_commit_warp<2, 2>(t_s, dX, dW1, ID64, 0, bar);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < K1 / 16; ++kk)
-                mma(t_s, dX + (uint64_t)(((kk >> 2) * S::TILE + (kk & 3) * 32) >> 4),
-                           dW1 + (uint64_t)(((kk >> 2) * 8192 + (kk & 3) * 32) >> 4), ID64, kk > 0);
-            commit(bar);
+                for (int kk = 0; kk < K1 / 16; ++kk)
+                    mma(t_s, dX + (uint64_t)(((kk >> 2) * S::TILE + (kk & 3) * 32) >> 4),
+                        dW1 + (uint64_t)(((kk >> 2) * 8192 + (kk & 3) * 32) >> 4), ID64, kk > 0);
+                commit(bar);
+            }
         }
         if (tile + tstride < p.n_tiles) fetch(tile + tstride, F);  // next tile's loads in flight
         wait_mma();
@@ -781,10 +789,15 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // Z2 = H1 W2^T + b2
         if (issuer) {
             tc_fence_after();
+            if constexpr (CH) {
+                mma_chain4_warp<2, 2>(t_s, dH1, dW2, ID64, 0);
+                mma1_commit_warp(t_s, dONES, dB2, ID64, 1, bar);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) mma(t_s, dH1 + 2 * kk, dW2 + 2 * kk, ID64, kk > 0);
-            mma(t_s, dONES, dB2, ID64, 1);
-            commit(bar);
+                for (int kk = 0; kk < 4; ++kk) mma(t_s, dH1 + 2 * kk, dW2 + 2 * kk, ID64, kk > 0);
+                mma(t_s, dONES, dB2, ID64, 1);
+                commit(bar);
+            }
         }
         wait_mma();
         NTC_TRACE(4);
@@ -808,10 +821,15 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // Y = H_last W3^T + b3
         if (issuer) {
             tc_fence_after();
+            if constexpr (CH) {
+                mma_chain4_warp<2, 2>(t_s, dHL, dW3, ID16, 0);
+                mma1_commit_warp(t_s, dONES, dB3, ID16, 1, bar);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) mma(t_s, dHL + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
-            mma(t_s, dONES, dB3, ID16, 1);
-            commit(bar);
+                for (int kk = 0; kk < 4; ++kk) mma(t_s, dHL + 2 * kk, dW3 + 2 * kk, ID16, kk > 0);
+                mma(t_s, dONES, dB3, ID16, 1);
+                commit(bar);
+            }
         }
         wait_mma();
         NTC_TRACE(6);
@@ -840,9 +858,15 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // ---- t5: dH_last = d3 W3
         if (issuer) {
             tc_fence_after();
-            mma(t_s, dD3, mW3, ID64_BT, 0);
-            commit(bar);
-            if (TRAIN_DWB_EARLY) {  // dW3/db3 += [X^T; H_last^T] delta3: its operands are final here
+            if constexpr (CH) {
+                mma1_commit_warp(t_s, dD3, mW3, ID64_BT, 0, bar);
+            } else {
+                mma(t_s, dD3, mW3, ID64_BT, 0);
+                commit(bar);
+            }
+            if (TRAIN_DWB_EARLY && CH) {
+                mma_chain8_warp<128, 128>(t_acc_b, mXHL, mD3, ID16_AB, !first);
+            } else if (TRAIN_DWB_EARLY) {  // dW3/db3 += [X^T; H_last^T] delta3: its operands are final here
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
                     mma(t_acc_b, mXHL + (uint64_t)(kk * 128), mD3 + (uint64_t)(kk * 128), ID16_AB,
@@ -921,10 +945,13 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // dH1 = d2 W2
         if (issuer) {
             tc_fence_after();
+            if constexpr (CH) {
+                mma_chain4_commit_warp<2, 128>(t_s, dG2, mW2, ID64_BT, 0, bar);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-                mma(t_s, dG2 + 2 * kk, mW2 + (uint64_t)(kk * 128), ID64_BT, kk > 0);
-            commit(bar);
+                for (int kk = 0; kk < 4; ++kk) mma(t_s, dG2 + 2 * kk, mW2 + (uint64_t)(kk * 128), ID64_BT, kk > 0);
+                commit(bar);
+            }
         }
         wait_mma();
         NTC_TRACE(10);
@@ -933,7 +960,12 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         sync_slot();
         NTC_TRACE(11);
         // dX = d1 W1 (latent columns) ; weight gradients accumulated in TMEM
-        if (issuer) {
+        if (issuer && CH) {  // the same groups, one asm block each
+            tc_fence_after();
+            mma_chain4_commit_warp<2, 128>(t_s, dG1, mW1, IDX_BT, 0, bar);
+            if (!TRAIN_DWB_EARLY) mma_chain8_warp<128, 128>(t_acc_b, mXHL, mD3, ID16_AB, !first);
+            mma_chain8_commit_warp<128, 128>(t_acc_a, mXH1, mG1, ID128_AB, !first, bar2);
+        } else if (issuer) {
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)

@@ -1,7 +1,8 @@
 """A/B timing between library builds (profiling helper, not product code):
   python tools/ab_decode.py [--train] LIB_A.so LIB_B.so [...] [--rounds R]
 alternates the builds in separate processes (one library per process), L2 flushed before each
-run, CUDA events: the headline chain decodes (c = 9, 16), or with --train the C4 step."""
+run, CUDA events: the headline chain decodes (c = 9, 16), or with --train the C4 step, --random
+the configs[2] random queries, --profiles the other Table 2 profiles and depth B."""
 import json
 import os
 import subprocess
@@ -79,11 +80,34 @@ t = _device_time(torch, lambda: ntc.ntc_decode_texels(mat, q, out), flush, 20)
 print(json.dumps({"random_c16": n / t / 1e9}))
 '''
 
+CHILD_PROFILES = r'''
+import sys, json, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2305_17105_b200 as ntc
+ntc.LIB_PATH = %r
+from bench import _device_time
+from paper_2305_17105_b200.synth import SEED_BASE, Profile, gen_codes, gen_weights_f16
+dev = torch.device("cuda", 0)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+out = {}
+for name, hm in (("ntc0.5", 1), ("ntc1.0", 1), ("ntc2.25", 1), ("ntc0.2", 2)):
+    d = Profile.named(name, 4096, 9, hm)
+    mat = ntc.Material(d, torch.from_numpy(gen_codes(SEED_BASE + 4, ntc.grid_list(d))).to(dev),
+                       torch.from_numpy(gen_weights_f16(SEED_BASE + 5, d.input_dim, 9, hm).view(np.int16)).to(dev))
+    T = ntc.ntc_chain_texels(d)
+    o = torch.empty(T * 9, dtype=torch.float16, device=dev)
+    t = _device_time(torch, lambda: ntc.ntc_decode_chain(mat, o), flush, 10)
+    out[name + ("" if hm == 1 else "_B")] = T / t / 1e9
+print(json.dumps(out))
+'''
+
 
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     rounds = int(sys.argv[sys.argv.index("--rounds") + 1]) if "--rounds" in sys.argv else 3
     child = CHILD_TRAIN if "--train" in sys.argv else (CHILD_RANDOM if "--random" in sys.argv else CHILD)
+    if "--profiles" in sys.argv:
+        child = CHILD_PROFILES
     libs = [a for a in args if a.endswith(".so")]
     res = {l: [] for l in libs}
     for _ in range(rounds):
