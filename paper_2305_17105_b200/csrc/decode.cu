@@ -131,6 +131,11 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, i
 #endif
 // 1: a steady-state loop without the per-phase idle checks while every context holds a tile
 // (A/B: neutral on the chain decode, -4% on random queries; off)
+// 1: the c = 16 query instantiation also gets the uniform-register MMA issue (A/B: random
+// queries 20.6 -> 20.2 Gtexel/s, off)
+#ifndef DECODE_UNI_QUERY
+#define DECODE_UNI_QUERY 0
+#endif
 #ifndef DECODE_WARP_ALL
 #define DECODE_WARP_ALL 0
 #endif
@@ -320,7 +325,7 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     // (more spills), so they keep the plain values.
     // uniform-register MMA issue (shuffled wg / TMEM base) and pipelined TMEM reads: mip
     // tiles and the compiled multi-material kernel; A/B-measured slower for the query kernel
-    constexpr bool UNI = TILED || (MULTI && CT != 0);
+    constexpr bool UNI = TILED || (MULTI && CT != 0) || (DECODE_UNI_QUERY && CT != 0);
     constexpr bool TMA = TILED && S::TMA_OUT;  // mip tiles: staged output, one bulk store per tile
     const int wg = UNI ? __shfl_sync(0xffffffffu, warp >> 2, 0) : warp >> 2, q = warp & 3, row = q * 32 + lane;
 

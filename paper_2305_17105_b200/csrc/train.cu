@@ -43,6 +43,11 @@ constexpr int MAX_BOXES = 256;
 #ifndef TRAIN_DWB_EARLY
 #define TRAIN_DWB_EARLY 0
 #endif
+// 1: the training input's G1 bilinear in packed fp16 (HFMA2) instead of fp32 + one rounding
+// (A/B: 63.2 vs 62.9 us per C4 step, off)
+#ifndef TRAIN_G1_H2
+#define TRAIN_G1_H2 0
+#endif
 #ifndef TRAIN_WARP_ISSUE  // see train_kernel
 #define TRAIN_WARP_ISSUE 2
 #endif
@@ -678,16 +683,42 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // to K1; both parts start on a 16-byte chunk (2 C0 is a multiple of 4 words)
         {
             constexpr int W0 = 2 * C0, W1N = K1 / 2 - 2 * C0;  // words of half 0 / half 1
-            constexpr int XW = W0 > W1N ? W0 : W1N;
-            uint32_t xw[XW];
-            if (h == 0) {  // G0 taps: the fp16 noisy latents are X
+            auto wait_pending = [&]() {
+                if (pending_w) {  // the previous tile's weight-gradient MMAs still read the tiles
+                    mbar_wait(bar2, phase2);
+                    phase2 ^= 1;
+                    tc_fence_after();
+                    pending_w = false;
+                }
+            };
+            if (h == 0) {  // G0 taps: the fp16 noisy latents are X, stored straight from the fetch
+                wait_pending();
 #pragma unroll
-                for (int i = 0; i < W0; ++i) xw[i] = F.v[i];
+                for (int ch = 0; ch < W0 / 4; ++ch)
+                    sts_row_chunk(tX + (uint32_t)(ch >> 3) * S::TILE, row, ch & 7, F.v[4 * ch], F.v[4 * ch + 1],
+                                  F.v[4 * ch + 2], F.v[4 * ch + 3]);
             } else {       // G1 bilinear in fp32 from the fp16 taps, rounded once; PE; LOD
+                uint32_t xw[W1N];
                 int tx[2], ty[2];
                 uint32_t ax, ay;
                 taps_g1(T, tx, ty, ax, ay);
                 const uint32_t wq[4] = {(16u - ax) * (16u - ay), ax * (16u - ay), (16u - ax) * ay, ax * ay};
+                if constexpr (TRAIN_G1_H2) {
+                    // packed fp16 bilinear: the weights (multiples of 1/256) are exact in fp16, each
+                    // HFMA2 step rounds once
+                    __half2 acc2[C1 / 2];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const __half2 w2 = __float2half2_rn((float)wq[t] * (1.0f / 256.0f));
+#pragma unroll
+                        for (int e = 0; e < C1 / 2; ++e) {
+                            const __half2 a2 = *reinterpret_cast<const __half2*>(&F.v[t * (C1 / 2) + e]);
+                            acc2[e] = t == 0 ? __hmul2(a2, w2) : __hfma2(a2, w2, acc2[e]);
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < C1 / 2; ++e) xw[e] = *reinterpret_cast<const uint32_t*>(&acc2[e]);
+                } else {
                 float acc[C1];
 #pragma unroll
                 for (int e = 0; e < C1; ++e) acc[e] = 0.0f;
@@ -703,6 +734,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                 }
 #pragma unroll
                 for (int e = 0; e < C1; e += 2) xw[e / 2] = h2u(acc[e], acc[e + 1]);
+                }
                 constexpr int PEW = C1 / 2;  // word index inside this half
                 xw[PEW + 0] = s_pe[4 * (T.x & 7) + 0];
                 xw[PEW + 1] = s_pe[4 * (T.x & 7) + 1];
@@ -713,18 +745,10 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
                 xw[PEW + 6] = p.lod_word;
 #pragma unroll
                 for (int e = PEW + 7; e < W1N; ++e) xw[e] = 0u;
-            }
-            if (pending_w) {  // the previous tile's weight-gradient MMAs still read the tiles
-                mbar_wait(bar2, phase2);
-                phase2 ^= 1;
-                tc_fence_after();
-                pending_w = false;
-            }
-            const int ch0 = h == 0 ? 0 : W0 / 4, nch = (h == 0 ? W0 : W1N) / 4;
+                wait_pending();
 #pragma unroll
-            for (int ch = 0; ch < XW / 4; ++ch) {
-                if (ch < nch) {
-                    const int g = ch0 + ch;  // chunk of the K1-wide row: atom g / 8, chunk g % 8
+                for (int ch = 0; ch < W1N / 4; ++ch) {
+                    const int g = W0 / 4 + ch;  // chunk of the K1-wide row: atom g / 8, chunk g % 8
                     sts_row_chunk(tX + (uint32_t)(g >> 3) * S::TILE, row, g & 7, xw[4 * ch], xw[4 * ch + 1],
                                   xw[4 * ch + 2], xw[4 * ch + 3]);
                 }
