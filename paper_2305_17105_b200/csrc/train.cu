@@ -490,17 +490,19 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     // each MMA (a single-thread waterfall around every tcgen05.mma); 1: the whole warp through
     // elect.sync, per MMA (measured slower: 65.5 vs 64.3 us); 2 (default): the whole warp, each
     // MMA group one asm block (one elect per group): 63.2 vs 64.4 us per C4 step (A/B, 3 rounds)
-    const bool issuer = (warp & 7) == slot * 2 && (TRAIN_WARP_ISSUE || lane == 0);
-    // TRAIN_WARP_ISSUE = 2: each MMA group of the depth-1, K1 = 64 kernel as one asm block
+    // TRAIN_WARP_ISSUE = 2: each MMA group of the depth-1, K1 = 64 kernel as one asm block; the
+    // other instantiations (one slot per CTA) keep the lane-0 issue
     constexpr bool CH = TRAIN_WARP_ISSUE >= 2 && HM == 1 && KA == 1;
+    constexpr bool WARP = TRAIN_WARP_ISSUE == 1 || CH;
+    const bool issuer = (warp & 7) == slot * 2 && (WARP || lane == 0);
     auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-        if constexpr (TRAIN_WARP_ISSUE)
+        if constexpr (WARP)
             mma_f16_ss_warp(d, a, b, id, acc);
         else
             mma_f16_ss(d, a, b, id, acc);
     };
     auto commit = [&](uint64_t* mb) {
-        if constexpr (TRAIN_WARP_ISSUE)
+        if constexpr (WARP)
             mma_commit_warp(mb);
         else
             mma_commit(mb);
