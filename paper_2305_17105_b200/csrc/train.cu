@@ -43,6 +43,11 @@ constexpr int MAX_BOXES = 256;
 #ifndef TRAIN_DWB_EARLY
 #define TRAIN_DWB_EARLY 0
 #endif
+// 1: prep_kernel is launched with programmatic dependent launch too (griddepcontrol.wait
+// before it reads the latents and weights the previous step's Adam wrote)
+#ifndef TRAIN_PREP_PDL
+#define TRAIN_PREP_PDL 1
+#endif
 // 1: the training input's G1 bilinear in packed fp16 (HFMA2) instead of fp32 + one rounding
 // (A/B: 63.2 vs 62.9 us per C4 step, off)
 #ifndef TRAIN_G1_H2
@@ -306,6 +311,9 @@ __device__ __forceinline__ void train_wimg_item_t(int i, const float* __restrict
 // t2: noisy = latent + U(-Q/2, Q/2) (one draw per latent per step), grad = 0, over the footprint
 __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
     pdl_launch_dependents();  // the training kernel's CTAs may start their prologue meanwhile
+    // launched programmatically after the previous step's Adam (TRAIN_PREP_PDL): its latents and
+    // weights are complete and visible past this point (a no-op for a plain launch)
+    pdl_wait();
     if ((int)blockIdx.x >= p.prep_blocks) {
         const int i = ((int)blockIdx.x - p.prep_blocks) * blockDim.x + threadIdx.x;
         if (p.wimg) {
@@ -1489,9 +1497,24 @@ __global__ void __launch_bounds__(256) reduce_adam_kernel(const __grid_constant_
                                                           const __grid_constant__ AdamParams a, int rblocks) {
     pdl_wait();  // the training kernel's partials and latent gradients are complete
     if ((int)blockIdx.x < rblocks) {
+        // the Adam state of this thread's weight is loaded together with the partials (one
+        // memory round trip instead of two)
+        const int iw = (int)blockIdx.x * 32 + (int)(threadIdx.x & 31);
+        const bool own = threadIdx.x < 32 && iw < a.P;
+        float pw = 0.0f, mw = 0.0f, vw = 0.0f;
+        if (own) {
+            pw = a.params[iw];
+            mw = a.m_par[iw];
+            vw = a.v_par[iw];
+        }
         int i;
         const float g = reduce_block(r, blockIdx.x, i);
-        if (i >= 0) adam_weight(a, i, g);
+        if (i >= 0) {
+            adam_one(pw, mw, vw, g, a.lr_w, a);
+            a.params[i] = pw;
+            a.m_par[i] = mw;
+            a.v_par[i] = vw;
+        }
         return;
     }
     adam_latent(a, (int64_t)(blockIdx.x - rblocks) * blockDim.x + threadIdx.x);
@@ -1948,7 +1971,15 @@ extern "C" ntc_status ntc_train_step(ntc_trainer* t, const ntc_desc* d, const nt
         pp.c = d->channels;
         pp.hm = d->hidden_mats;
         pp.wimg = t->wimg;
-        prep_kernel<<<pp.prep_blocks + (wimg_items(pp.hm, pp.D + 1 > 64 ? 2 : 1) + 255) / 256, 256, 0, st>>>(pp);
+        {
+            const int pg = pp.prep_blocks + (wimg_items(pp.hm, pp.D + 1 > 64 ? 2 : 1) + 255) / 256;
+            if (TRAIN_PREP_PDL) {  // overlaps this launch with the previous kernel's tail
+                const cudaError_t e = launch_pdl(prep_kernel, pg, 256, 0, st, pp);
+                if (e != cudaSuccess) return api_fail(NTC_ERR_CUDA, cudaGetErrorString(e));
+            } else {
+                prep_kernel<<<pg, 256, 0, st>>>(pp);
+            }
+        }
         // t1, t3-t7
         TrainParams tp;
         memset(&tp, 0, sizeof tp);
