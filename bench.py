@@ -63,6 +63,26 @@ def _ncu_metric(kernel, name):
         return None
 
 
+def _ncu_instructions(kernel):
+    """warp instructions per launch of `kernel` from the committed ncu summary (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return float(json.load(f)["kernels"][kernel]["instructions_per_launch"])
+    except Exception:
+        return None
+
+
+def _issue_ceiling(torch, dev, instr_per_launch, units, sm_mhz):
+    """The instruction-issue roofline of a kernel: every SM sub-partition issuing one warp
+    instruction per cycle (4 per SM) at the sampled SM clock, divided by the kernel's warp
+    instructions per unit (ncu).  Returns (units/s ceiling, thread instructions per unit)."""
+    if not instr_per_launch or not sm_mhz:
+        return None, None
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    per_unit = instr_per_launch / units
+    return 4 * sms * sm_mhz * 1e6 / per_unit, 32 * per_unit
+
+
 def _ncu_traffic(kernel):
     """dram read+write bytes per launch of `kernel` from the committed ncu summary (or None)."""
     try:
@@ -267,6 +287,16 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": args.steps + launches["train"],
         "clocks": clk.report(),
     })
+    # the bound that actually binds the decode: instruction issue on the ALU work
+    # around the contractions -- the texel rate at one warp instruction per sub-partition per
+    # cycle, and the fraction of it reached (diagnostic; `frac` above stays the tensor roofline)
+    ceil_t, ipt = _issue_ceiling(torch, dev, _ncu_instructions("decode"), T,
+                                 res["clocks"].get("sm_mhz") or res["clocks"].get("sm_max_mhz"))
+    if ceil_t:
+        res["roofline"]["diagnostics"].update({
+            "thread_instructions_per_texel": round(ipt, 1),
+            "issue_ceiling_gtexel_s": round(ceil_t / 1e9, 2),
+            "frac_of_issue_ceiling": round(res["value"] / (ceil_t / 1e9 * world), 4)})
     if train is not None:
         B = 4 * 256 * 256
         tflops = train_flops_per_texel(d) * B / (trn / args.steps) / 1e12
