@@ -133,6 +133,12 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t taddr, uint32_t tile, i
 // (A/B: neutral on the chain decode, -4% on random queries; off)
 // 1: the c = 16 query instantiation also gets the uniform-register MMA issue (A/B: random
 // queries 20.6 -> 20.2 Gtexel/s, off)
+// 1: the lane quarter goes through a shuffle as well (uniform-register instantiations).  A/B, 3
+// rounds: 4K chain c = 9 32.33 -> 33.65 Gtexel/s, c = 16 32.30 -> 33.95, NTC 0.5 / 1.0 / 2.25
+// 23.1 / 28.7 / 25.5 -> 25.3 / 30.8 / 28.2; ptxas: 114 -> 96 registers, R2UR 50 -> 4
+#ifndef DECODE_UNI_Q
+#define DECODE_UNI_Q 1
+#endif
 #ifndef DECODE_UNI_QUERY
 #define DECODE_UNI_QUERY 0
 #endif
@@ -327,7 +333,10 @@ __device__ __forceinline__ void decode_body(const DecodeParams& p, const MultiTa
     // tiles and the compiled multi-material kernel; A/B-measured slower for the query kernel
     constexpr bool UNI = TILED || (MULTI && CT != 0) || (DECODE_UNI_QUERY && CT != 0);
     constexpr bool TMA = TILED && S::TMA_OUT;  // mip tiles: staged output, one bulk store per tile
-    const int wg = UNI ? __shfl_sync(0xffffffffu, warp >> 2, 0) : warp >> 2, q = warp & 3, row = q * 32 + lane;
+    // (the lane quarter too, so the issuing-warp test `q == C.iq` is provably warp-uniform and the
+    // elect.sync blocks need no divergence check)
+    const int wg = UNI ? __shfl_sync(0xffffffffu, warp >> 2, 0) : warp >> 2;
+    const int q = (UNI && DECODE_UNI_Q) ? __shfl_sync(0xffffffffu, warp & 3, 0) : warp & 3, row = q * 32 + lane;
 
     if (!MULTI)
         for (uint32_t i = tid; i < S::WIMG / 16; i += blockDim.x) reinterpret_cast<uint4*>(s_w)[i] = p.wimg[i];

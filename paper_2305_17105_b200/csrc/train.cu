@@ -53,6 +53,10 @@ constexpr int MAX_BOXES = 256;
 #ifndef TRAIN_G1_H2
 #define TRAIN_G1_H2 0
 #endif
+// 1 (see train_kernel): A/B, 3 rounds: C4 step 62.9 -> 60.9 us; ptxas: R2UR 56 -> 4, VOTEU 75 -> 6
+#ifndef TRAIN_UNI_WARP
+#define TRAIN_UNI_WARP 1
+#endif
 #ifndef TRAIN_WARP_ISSUE  // see train_kernel
 #define TRAIN_WARP_ISSUE 2
 #endif
@@ -442,7 +446,12 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
 #endif
     // slot and the TMEM base go through a shuffle: provably warp-uniform, so the MMA-issuing
     // thread keeps its descriptors in uniform registers (no R2UR waterfall per tcgen05.mma)
-    const int slot = __shfl_sync(0xffffffffu, warp >> 3, 0), h = (warp >> 2) & 1, q = warp & 3, row = q * 32 + lane;
+    // (with TRAIN_UNI_WARP the column half and lane quarter too: every warp-role test -- the
+    // issuing warp, the half -- is then provably warp-uniform, which lets ptxas keep the MMA
+    // operands and the role-dependent addresses on the uniform datapath)
+    const int slot = __shfl_sync(0xffffffffu, warp >> 3, 0);
+    const int wrole = TRAIN_UNI_WARP ? __shfl_sync(0xffffffffu, warp & 7, 0) : warp & 7;
+    const int h = wrole >> 2, q = wrole & 3, row = q * 32 + lane;
     const int c = CT ? CT : p.c;
 
     // ---- weight images (fp16, built once per step by the trailing blocks of prep_kernel; the
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     // other instantiations (one slot per CTA) keep the lane-0 issue
     constexpr bool CH = TRAIN_WARP_ISSUE >= 2 && HM == 1 && KA == 1;
     constexpr bool WARP = TRAIN_WARP_ISSUE == 1 || CH;
-    const bool issuer = (warp & 7) == slot * 2 && (WARP || lane == 0);
+    const bool issuer = wrole == slot * 2 && (WARP || lane == 0);
     auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
         if constexpr (WARP)
             mma_f16_ss_warp(d, a, b, id, acc);
