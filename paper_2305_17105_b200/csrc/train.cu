@@ -507,9 +507,8 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
     // each MMA (a single-thread waterfall around every tcgen05.mma); 1: the whole warp through
     // elect.sync, per MMA (measured slower: 65.5 vs 64.3 us); 2 (default): the whole warp, each
     // MMA group one asm block (one elect per group): 63.2 vs 64.4 us per C4 step (A/B, 3 rounds)
-    // TRAIN_WARP_ISSUE = 2: each MMA group of the depth-1, K1 = 64 kernel as one asm block; the
-    // other instantiations (one slot per CTA) keep the lane-0 issue
-    constexpr bool CH = TRAIN_WARP_ISSUE >= 2 && HM == 1 && KA == 1;
+    // TRAIN_WARP_ISSUE = 2: each MMA group as one asm block (every profile and depth)
+    constexpr bool CH = TRAIN_WARP_ISSUE >= 2;
     constexpr bool WARP = TRAIN_WARP_ISSUE == 1 || CH;
     const bool issuer = wrole == slot * 2 && (WARP || lane == 0);
     auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -779,8 +778,13 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
         // ---- t3: forward.  Z1 = X W1^T (+b1)
         if (issuer) {
             tc_fence_after();
-            if constexpr (CH) {
+            if constexpr (CH && KA == 1) {
                 mma_chain4_commit_warp<2, 2>(t_s, dX, dW1, ID64, 0, bar);
+            } else if constexpr (CH) {  // K1 = 80 / 96: atom 0's chain, then atom 1's one or two steps
+                mma_chain4_warp<2, 2>(t_s, dX, dW1, ID64, 0);
+                constexpr uint64_t A1 = S::TILE >> 4, B1 = 8192 >> 4;
+                if constexpr (K1 / 16 == 6) mma_f16_ss_warp(t_s, dX + A1, dW1 + B1, ID64, 1);
+                mma1_commit_warp(t_s, dX + A1 + (K1 / 16 == 6 ? 2 : 0), dW1 + B1 + (K1 / 16 == 6 ? 2 : 0), ID64, 1, bar);
             } else {
 #pragma unroll
                 for (int kk = 0; kk < K1 / 16; ++kk)
@@ -849,10 +853,15 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             sync_slot();
             if (issuer) {
                 tc_fence_after();
+                if constexpr (CH) {
+                    mma_chain4_warp<2, 2>(t_s, dH2, dW2B, ID64, 0);
+                    mma1_commit_warp(t_s, dONES, dB2B, ID64, 1, bar);
+                } else {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) mma(t_s, dH2 + 2 * kk, dW2B + 2 * kk, ID64, kk > 0);
-                mma(t_s, dONES, dB2B, ID64, 1);
-                commit(bar);
+                    for (int kk = 0; kk < 4; ++kk) mma(t_s, dH2 + 2 * kk, dW2B + 2 * kk, ID64, kk > 0);
+                    mma(t_s, dONES, dB2B, ID64, 1);
+                    commit(bar);
+                }
             }
             wait_mma();
             hidden_epilogue(tH3, tG3);
@@ -974,10 +983,14 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             sync_slot();
             if (issuer) {
                 tc_fence_after();
+                if constexpr (CH) {
+                    mma_chain4_commit_warp<2, 128>(t_s, dG3, mW2B, ID64_BT, 0, bar);
+                } else {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    mma(t_s, dG3 + 2 * kk, mW2B + (uint64_t)(kk * 128), ID64_BT, kk > 0);
-                commit(bar);
+                    for (int kk = 0; kk < 4; ++kk)
+                        mma(t_s, dG3 + 2 * kk, mW2B + (uint64_t)(kk * 128), ID64_BT, kk > 0);
+                    commit(bar);
+                }
             }
             wait_mma();
             delta_epilogue(tG2);
@@ -1007,7 +1020,13 @@ __global__ void __launch_bounds__(TrainSmemT<HM, TrainGeom<P>::KA>::SLOTS * 256,
             tc_fence_after();
             mma_chain4_commit_warp<2, 128>(t_s, dG1, mW1, IDX_BT, 0, bar);
             if (!TRAIN_DWB_EARLY) mma_chain8_warp<128, 128>(t_acc_b, mXHL, mD3, ID16_AB, !first);
-            mma_chain8_commit_warp<128, 128>(t_acc_a, mXH1, mG1, ID128_AB, !first, bar2);
+            if constexpr (HM == 2) mma_chain8_warp<128, 128>(t_acc_m, mXH2, mG3, ID64_AB, !first);
+            if constexpr (KA == 1) {
+                mma_chain8_commit_warp<128, 128>(t_acc_a, mXH1, mG1, ID128_AB, !first, bar2);
+            } else {
+                mma_chain8_warp<128, 128>(t_acc_a + 64, mXH1, mG2, ID64_AB, !first);
+                mma_chain8_commit_warp<128, 128>(t_acc_a, mXX, mG1, ID64_AB, !first, bar2);
+            }
         } else if (issuer) {
             tc_fence_after();
 #pragma unroll
