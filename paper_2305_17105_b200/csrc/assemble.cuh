@@ -69,31 +69,42 @@ __device__ __forceinline__ Cell<BYTES> load_cell(const uint8_t* base, int64_t id
 // masked, SH + B <= 10): half(0x6400 | code << SH) = 1024 + code 2^SH; one HFMA2 with the
 // power-of-2 scale Q / 2^SH gives (code - N/2 + 1) / N exactly (R10): the
 // product is exact and the result is representable, so the single rounding is exact.
-template <int B, int SH = 0>
+template <int B, int SH = 0, bool MAGIC_SET = false>
 __device__ __forceinline__ uint32_t dequant2(uint32_t lanes) {
     static_assert(SH + B <= 10, "code bits must stay inside the fp16 mantissa");
     constexpr float Q = 1.0f / (float)(1 << B);
     constexpr float OFF = (float)((1 << B) / 2 - 1);
     constexpr float SC = Q / (float)(1 << SH);
-    const uint32_t v = lanes | 0x64006400u;
+    // MAGIC_SET: the caller already ORed in 0x64006400 (one fused lop3 with its mask)
+    const uint32_t v = MAGIC_SET ? lanes : lanes | 0x64006400u;
     __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&v), __float2half2_rn(SC),
                         __float2half2_rn(-(1024.0f / (float)(1 << SH) + OFF) * Q));
     return *reinterpret_cast<uint32_t*>(&r);
 }
 
+// (y & mask) | 0x64006400 as ONE lop3 (ptxas splits it into two LOP3s when both constants are
+// immediates); dequant2<..., true> then skips its own OR
+__device__ __forceinline__ uint32_t mask_or_magic(uint32_t y, uint32_t mask) {
+    uint32_t v;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(v) : "r"(y), "r"(mask), "r"(0x64006400u));
+    return v;
+}
+
 // 4-bit codes: split a 32-bit word of `nch` channels into lane pairs (bits 0-3 | 16-19)
-template <int NCH>
+// (MAGIC: each lane pair already ORed with the fp16 magic 0x6400 by the same lop3)
+template <int NCH, bool MAGIC = false>
 __device__ __forceinline__ void nib_lanes(uint32_t w, uint32_t* out) {
+    auto m = [](uint32_t v) { return MAGIC ? mask_or_magic(v, 0x000F000Fu) : v & 0x000F000Fu; };
     if constexpr (NCH == 8) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) out[q] = (w >> (4 * q)) & 0x000F000Fu;  // (q, q+4)
+        for (int q = 0; q < 4; ++q) out[q] = m(w >> (4 * q));  // (q, q+4)
     } else if constexpr (NCH == 4) {
-        const uint32_t y = __byte_perm(w, 0u, 0x4140);                     // [b0, 0, b1, 0]
-        out[0] = y & 0x000F000Fu;                                          // (0, 2)
-        out[1] = (y >> 4) & 0x000F000Fu;                                   // (1, 3)
+        const uint32_t y = __byte_perm(w, 0u, 0x4140);       // [b0, 0, b1, 0]
+        out[0] = m(y);                                        // (0, 2)
+        out[1] = m(y >> 4);                                   // (1, 3)
     } else {
         const uint32_t y = w | (w << 12);
-        out[0] = y & 0x000F000Fu;                                          // (0, 1)
+        out[0] = m(y);                                        // (0, 1)
     }
 }
 
@@ -191,10 +202,10 @@ __device__ __forceinline__ void g0_words_c8b2(const uint32_t (&cell)[4], uint32_
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const uint32_t y = __byte_perm(cell[t], 0u, 0x4140);
-        w[4 * t + 0] = dequant2<2, 0>(y & 0x00030003u);
-        w[4 * t + 1] = dequant2<2, 2>(y & 0x000C000Cu);
-        w[4 * t + 2] = dequant2<2, 4>(y & 0x00300030u);
-        w[4 * t + 3] = dequant2<2, 6>(y & 0x00C000C0u);
+        w[4 * t + 0] = dequant2<2, 0, true>(mask_or_magic(y, 0x00030003u));
+        w[4 * t + 1] = dequant2<2, 2, true>(mask_or_magic(y, 0x000C000Cu));
+        w[4 * t + 2] = dequant2<2, 4, true>(mask_or_magic(y, 0x00300030u));
+        w[4 * t + 3] = dequant2<2, 6, true>(mask_or_magic(y, 0x00C000C0u));
     }
 }
 
@@ -285,32 +296,33 @@ __device__ __forceinline__ void assemble_words(const DecodeParams& p, const uint
         for (int t = 0; t < 4; ++t) {
             const uint32_t y = __byte_perm(f.g0[t].w[0], 0u, 0x4140);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) w[4 * t + k] = dequant2<2>((y >> (2 * k)) & 0x00030003u);
+            for (int k = 0; k < 4; ++k) w[4 * t + k] = dequant2<2, 0, true>(mask_or_magic(y >> (2 * k), 0x00030003u));
         }
 #pragma unroll
         for (int pi = 0; pi < 2; ++pi) {
             const uint32_t y = __byte_perm(f.g0[2 * pi].w[0], f.g0[2 * pi + 1].w[0], 0x7672);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) w[16 + 4 * pi + k] = dequant2<2>((y >> (2 * k)) & 0x00030003u);
+            for (int k = 0; k < 4; ++k)
+                w[16 + 4 * pi + k] = dequant2<2, 0, true>(mask_or_magic(y >> (2 * k), 0x00030003u));
         }
     } else if constexpr (P::C0 == 12 && P::B0 == 4) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             uint32_t l[6];
-            nib_lanes<8>(f.g0[t].w[0], l);
-            nib_lanes<4>(f.g0[t].w[1], l + 4);
+            nib_lanes<8, true>(f.g0[t].w[0], l);
+            nib_lanes<4, true>(f.g0[t].w[1], l + 4);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) w[6 * t + k] = dequant2<4>(l[k]);
+            for (int k = 0; k < 6; ++k) w[6 * t + k] = dequant2<4, 0, true>(l[k]);
         }
     } else {
         static_assert(P::C0 == 16 && P::B0 == 4, "unsupported G0 profile");
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             uint32_t l[8];
-            nib_lanes<8>(f.g0[t].w[0], l);
-            nib_lanes<8>(f.g0[t].w[1], l + 4);
+            nib_lanes<8, true>(f.g0[t].w[0], l);
+            nib_lanes<8, true>(f.g0[t].w[1], l + 4);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) w[8 * t + k] = dequant2<4>(l[k]);
+            for (int k = 0; k < 8; ++k) w[8 * t + k] = dequant2<4, 0, true>(l[k]);
         }
     }
     // ---- G1 bilinear, PE, LOD
